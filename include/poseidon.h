@@ -1,0 +1,226 @@
+/*
+ * poseidon.h — C ABI of the B200-native Poseidon per-layer gradient synchronisation.
+ *
+ * Paper: Zhang et al., "Poseidon: An Efficient Communication Architecture for Distributed Deep
+ * Learning on GPU Clusters", USENIX ATC'17 (arXiv 1706.03292). Citations below are
+ * `PAPER:<line> §<section>` into that text and `SURVEY §8(x)` into
+ * SURVEY.md, whose §8 is the hot-path contract this header implements.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", plain pointers and integer sizes; no CUDA, NCCL or torch types. A `stream` is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream); an `event` is a cudaEvent_t.
+ *  - All sizes are int64_t element counts unless stated. Device pointers are CALLER-OWNED and must
+ *    stay valid and unmodified (except by the library) until the operation has completed in
+ *    stream order. The library never frees caller memory.
+ *  - FC layer notation: W is M x N row-major fp32 with M = out_features and
+ *    N = in_features (the nn.Linear.weight layout); b has M entries. Per-sample sufficient factors
+ *    (§2.1): u = dL/dy in R^M, v = x in R^N. A worker's K samples are stored as
+ *    u: K x M row-major, v: K x N row-major (autograd's grad_output and saved input).
+ *  - Update rule: every entry point computes W += alpha * G where G is the summed LOSS gradient
+ *    over all P workers (Eq. 2). alpha carries the learning rate, the sign and any
+ *    normalisation (readings S5, S6); the library never divides by K or P.
+ *  - Errors: synchronous validation returns < 0 (POS_E*) and sets a thread-local message readable
+ *    with pos_last_error(). Asynchronous CUDA/NCCL failures are sticky per context and returned by
+ *    pos_get_async_error() and by the next call on that context.
+ *  - Threading: one host thread drives a context at a time (replaces the paper's CPU thread pool,
+ *    PAPER:266 §4.1).
+ *  - Determinism: identical inputs give bitwise-identical W on every rank, for both schemes, and
+ *    between WFBP and sequential scheduling (no atomics; fixed k order).
+ */
+#ifndef POSEIDON_H
+#define POSEIDON_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pos_ctx pos_ctx;
+typedef struct pos_sched pos_sched;
+
+/* Communication schemes (§3.2, Table 1). ADAM only for pos_cost_elems. */
+enum { POS_SCHEME_PS = 0, POS_SCHEME_SFB = 1, POS_SCHEME_ADAM = 2 };
+/* Layer kinds for Algorithm 1: FC is decomposable; DENSE = CONV/BN, "indecomposable" -> PS. */
+enum { POS_KIND_FC = 0, POS_KIND_DENSE = 1 };
+/* Node roles of Table 1 columns. */
+enum { POS_ROLE_SERVER = 0, POS_ROLE_WORKER = 1, POS_ROLE_BOTH = 2 };
+/* Factor COMPUTE dtype of the SFB reconstruction (what is gathered and fed to the contraction):
+ *   BF16: factors rounded to bf16 (RNE), tcgen05 kind::f16, fp32 accumulate in TMEM.
+ *   TF32: factors kept fp32, tcgen05 kind::tf32 (tensor core rounds to tf32), fp32 accumulate.
+ *   F32 : factors kept fp32, exact fp32 FFMA contraction (SIMT), fp32 accumulate. */
+enum { POS_DT_BF16 = 0, POS_DT_TF32 = 1, POS_DT_F32 = 2 };
+/* Storage dtype of the caller's u / v buffers. */
+enum { POS_IN_BF16 = 0, POS_IN_F32 = 1 };
+/* Error codes. */
+enum {
+  POS_OK = 0, POS_EINVAL = -1, POS_ESTATE = -2, POS_ECUDA = -3, POS_ENCCL = -4,
+  POS_ENOMEM = -5, POS_EUNSUPPORTED = -6
+};
+/* pos_sched_create flags */
+enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2 };
+
+/* ABI version (major * 100 + minor). */
+int pos_version(void);
+/* Message of the last < 0 return on this host thread ("" if none). Never NULL. */
+const char* pos_last_error(void);
+
+/* ======================================================================================
+ * Pure host functions (no context, no GPU).
+ * ====================================================================================== */
+
+/* Algorithm 1 BestScheme for an FC layer with P1 = P2 = P (every GPU is both a
+ * worker and a PS shard; reading S1). Returns POS_SCHEME_SFB iff
+ *     2K(P-1)(M+N) <= 2MN(2P-2)/P,
+ * evaluated exactly by 128-bit cross-multiplication (reading S4; tie -> SFB, reading S2; P = 1 ->
+ * SFB, reading S8). K is the per-worker batch (reading S3). M, N, K, P >= 1 else POS_EINVAL. */
+int pos_choose_scheme(int64_t M, int64_t N, int64_t K, int32_t P);
+
+/* General Algorithm 1 with separate worker count P1 and server count P2 and a layer kind.
+ * kind = POS_KIND_DENSE always returns POS_SCHEME_PS. */
+int pos_choose_scheme2(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P1, int32_t P2);
+
+/* Table 1 cost in ELEMENTS as an exact reduced rational num/den (den >= 1).
+ * scheme: POS_SCHEME_{PS,SFB,ADAM}; role: POS_ROLE_{SERVER,WORKER,BOTH}. SFB with role SERVER or
+ * BOTH is "N/A" in Table 1 -> POS_EUNSUPPORTED. Overflow of uint64 -> POS_EINVAL. */
+int pos_cost_elems(int32_t scheme, int32_t role, int64_t M, int64_t N, int64_t K,
+                   int32_t P1, int32_t P2, uint64_t* num, uint64_t* den);
+
+/* PS shard table ("partition ... as equally as possible"; reading S9): contiguous
+ * shards of stride S = ceil(n / (64 P)) * 64 elements. Returns S (> 0) or < 0 on n < 1 or P < 1. */
+int64_t pos_shard_stride(int64_t n, int32_t P);
+/* Rank r owns [min(n, r S), min(n, (r+1) S)). */
+int pos_shard_range(int64_t n, int32_t P, int32_t r, int64_t* begin, int64_t* end);
+/* Elements a caller must allocate for a PS layer's W and grad buffers: P * S. */
+int64_t pos_padded_size(int64_t n, int32_t P);
+/* Row length (elements) of the library's gathered factor layout for an FC layer:
+ * M_pad + N_pad with M_pad = ceil(M/8)*8, N_pad = ceil(N/8)*8 (16-byte TMA row rule). */
+int64_t pos_factor_row_elems(int64_t M, int64_t N);
+
+/* ======================================================================================
+ * Context: owns the NCCL communicator, a comm stream, a stream pool and scratch buffers.
+ * Created on the CURRENT CUDA device of the calling thread.
+ * ====================================================================================== */
+
+/* Fill out_128B (128 bytes) with an ncclUniqueId. Call on rank 0, broadcast, then pos_init. */
+int pos_get_unique_id(void* out_128B);
+/* Collective over `world` processes (one per GPU); blocks until all ranks have joined. */
+int pos_init(const void* nccl_unique_id_128B, int32_t world, int32_t rank, pos_ctx** out);
+/* Single-GPU context simulating P_sim workers (no NCCL): for the pos_sim_* entry points and for
+ * P_sim = 1 real single-GPU use. */
+int pos_init_local(int32_t P_sim, pos_ctx** out);
+int pos_finalize(pos_ctx* ctx);
+int pos_world(const pos_ctx* ctx);
+int pos_rank(const pos_ctx* ctx);
+/* Sticky asynchronous CUDA/NCCL error (POS_OK if none). */
+int pos_get_async_error(pos_ctx* ctx);
+/* Cap the number of CTAs of the persistent SFB reconstruction kernel (0 = one per SM). Lets the
+ * sync leave SMs to the concurrent backward pass (SURVEY §7 hard part 3). */
+int pos_set_max_ctas(pos_ctx* ctx, int32_t max_ctas);
+
+/* ======================================================================================
+ * Kernel-level building blocks (stream-ordered, asynchronous). Exposed for tests and callers
+ * that bring their own transport.
+ * ====================================================================================== */
+
+/* A2 — SFB factor pack ("transformation between SFs and gradients"): write the K rows
+ *   slot[k][0 .. M_pad)            = dtype(u[k][0..M)), zero in [M, M_pad)
+ *   slot[k][M_pad .. M_pad+N_pad)  = dtype(v[k][0..N)), zero in the pad
+ * slot: device, K * pos_factor_row_elems(M,N) elements of bf16 (dtype BF16) or fp32 (TF32/F32),
+ * 16-byte aligned. u, v: device, in_dtype storage, any alignment. */
+int pos_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
+                     const void* u, const void* v, void* slot, void* stream);
+
+/* A4 + A4b — SFB reconstruct-and-apply (Eq. 2):
+ *   W[m][n] = (accumulate ? W[m][n] : 0) + alpha * sum_{j < KP} U[j][m] * V[j][n]
+ *   b[m]    = (accumulate ? b[m]    : 0) + alpha * sum_{j < KP} U[j][m]        (if b != NULL)
+ * where row j of the gathered buffer G (KP rows of pos_factor_row_elems(M,N) elements, packed by
+ * pos_pack_factors, worker-major: j = p*K + k) holds [u_j | v_j]. W: device fp32, row stride ldw
+ * elements (ldw >= N). BF16/TF32 run the tcgen05/TMEM/TMA kernel when ldw % 4 == 0 and W is
+ * 16-byte aligned (else the SIMT kernel); F32 always runs the exact SIMT FFMA kernel. The k order
+ * is fixed, so results are bitwise reproducible. */
+int pos_reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
+                          int32_t accumulate, float* W, int64_t ldw, float* b, float alpha,
+                          void* stream);
+
+/* A7 — PS shard apply (PAPER:107 step (2) "apply (+)"): W[i] += alpha * g[i], 0 <= i < count.
+ * 16-byte vectorised when both pointers are 16-byte aligned. */
+int pos_ps_apply(const float* g, float* W, int64_t count, float alpha, void* stream);
+
+/* ======================================================================================
+ * One-shot per-layer synchronisation (stream-ordered on `stream`, returns after enqueue).
+ * These share one context workspace: issue them on one stream (or serialise them).
+ * ====================================================================================== */
+
+/* SFB: pack this rank's factors, ncclAllGather them over the
+ * context's communicator, then W += alpha * U^T V over all K*P samples (and b += alpha*colsum(U)).
+ * At world 1 there is no collective. u, v: device, K x M / K x N, in_dtype. */
+int pos_sync_layer_sfb(pos_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
+                       int32_t dtype, const void* u, const void* v, float* W, float* b,
+                       float alpha, void* stream);
+
+/* PS for a dense (CONV/BN) layer of n parameters:
+ * zero grad[n, P*S) (A5), ncclReduceScatter(sum) in place so rank r holds sum_p g_p on its shard
+ * (A6), W[shard r] += alpha * that sum (A7), ncclAllGather(W) in place (A8).
+ * grad, W: device fp32 with >= pos_padded_size(n, P) elements, 16-byte aligned; W[n..P*S) is
+ * scratch. After completion every rank holds identical W[0..n). */
+int pos_sync_layer_ps(pos_ctx* ctx, int64_t n, float* grad, float* W, float alpha, void* stream);
+
+/* PS for an FC layer (scheme forced to PS, or Algorithm 1 chose PS): the local dense gradient
+ * G_r = U_r^T V_r (and colsum(U_r) for the bias) is formed by the reconstruction kernel in
+ * overwrite mode into grad, then synchronised as a dense layer of n = M*N (+ M if has_bias)
+ * parameters laid out [W (M x N row-major) | b (M)]. Wb, grad: >= pos_padded_size(n, P) fp32. */
+int pos_sync_layer_fc_ps(pos_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
+                         int32_t dtype, const void* u, const void* v, float* grad, float* Wb,
+                         int32_t has_bias, float alpha, void* stream);
+
+/* Simulated P workers on one GPU (context from pos_init_local(P)). The per-worker inputs are host
+ * arrays of P device pointers; the library plays the collective's role by packing every worker's
+ * factors into its slot of the gather buffer (SFB), or summing the P gradients in worker order
+ * (PS). Results are what every rank would hold after the real synchronisation. */
+int pos_sim_sync_layer_sfb(pos_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
+                           int32_t dtype, const void* const* u, const void* const* v, float* W,
+                           float* b, float alpha, void* stream);
+int pos_sim_sync_layer_ps(pos_ctx* ctx, int64_t n, const float* const* grads, float* W,
+                          float alpha, void* stream);
+
+/* ======================================================================================
+ * WFBP scheduler (§3.1, Algorithm 2, vector C PAPER:273-275).
+ * One record per layer ("syncer"). Per iteration:
+ *   pos_sched_begin  -> C := 0
+ *   for l = L..1 as backward produces them:
+ *     FC  : pos_sched_factors_ready(l, u, v, stream)   (after b^l read W: u, v ready, W free)
+ *     DENSE: pos_sched_grad_ready(l, stream)           (after dW of layer l is in grad)
+ *   pos_sched_end(consumer)   -> consumer stream waits until all of C is 1 (Alg. 2 L8)
+ * Each trigger records an event on the caller's `stream` and enqueues the layer's sync on the
+ * library's streams (one comm stream, a pool of apply streams), so s^l overlaps b^i, i < l.
+ * Layer indices are 0-based in forward order. Buffers passed at add time must outlive the
+ * scheduler. Calls return POS_ESTATE on misuse (trigger twice, end before all triggered,
+ * add after begin).
+ * ====================================================================================== */
+int pos_sched_create(pos_ctx* ctx, int32_t n_layers, int32_t flags, pos_sched** out);
+/* FC layer. force_scheme = -1 applies Algorithm 1; else POS_SCHEME_SFB / POS_SCHEME_PS.
+ * If the scheme is PS: b must be NULL or W + M*N (one flat [W|b] buffer), and W and grad must
+ * have pos_padded_size(M*N (+M), P) elements. Returns the scheme (>= 0) or < 0. */
+int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
+                     int32_t dtype, float* W, float* b, float* grad, int32_t force_scheme);
+/* DENSE layer of n parameters: W and grad with pos_padded_size(n, P) elements. Returns PS. */
+int pos_sched_add_dense(pos_sched* s, int32_t l, int64_t n, float* W, float* grad);
+int pos_sched_begin(pos_sched* s, float alpha);
+int pos_sched_factors_ready(pos_sched* s, int32_t l, const void* u, const void* v, void* stream);
+int pos_sched_grad_ready(pos_sched* s, int32_t l, void* stream);
+/* Per-layer RAW gate: `consumer` waits until layer l's parameters are applied (for f^l of the
+ * next iteration; the cross-iteration overlap of PAPER:158). */
+int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer);
+int pos_sched_end(pos_sched* s, void* consumer);
+/* Query: the scheme chosen for layer l. */
+int pos_sched_scheme(pos_sched* s, int32_t l);
+/* With POS_SCHED_TIMING: device milliseconds of the last iteration's pack, collective(s) and
+ * apply stages of layer l (synchronises on the layer's completion). */
+int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, float* apply_ms);
+int pos_sched_destroy(pos_sched* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POSEIDON_H */

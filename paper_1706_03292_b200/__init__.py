@@ -1,0 +1,274 @@
+"""paper_1706_03292_b200 — B200-native Poseidon per-layer gradient synchronisation.
+
+Thin Python binding over libposeidon.so (include/poseidon.h). Names follow the C ABI
+(`pos_choose_scheme`, `pos_sync_layer_sfb`, ...); the classes below only marshal torch tensors to
+raw device pointers and CUDA stream handles. Every step of the synchronisation runs in the
+library's CUDA kernels and NCCL calls; there is no CPU fallback.
+
+Paper: Zhang et al., "Poseidon", USENIX ATC'17 (arXiv 1706.03292).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from ._lib import lib, LIB_PATH
+
+POS_SCHEME_PS, POS_SCHEME_SFB, POS_SCHEME_ADAM = 0, 1, 2
+POS_KIND_FC, POS_KIND_DENSE = 0, 1
+POS_ROLE_SERVER, POS_ROLE_WORKER, POS_ROLE_BOTH = 0, 1, 2
+POS_DT_BF16, POS_DT_TF32, POS_DT_F32 = 0, 1, 2
+POS_IN_BF16, POS_IN_F32 = 0, 1
+POS_OK, POS_EINVAL, POS_ESTATE, POS_ECUDA, POS_ENCCL, POS_ENOMEM, POS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL = 1, 2
+
+DTYPES = {"bf16": POS_DT_BF16, "tf32": POS_DT_TF32, "f32": POS_DT_F32}
+SCHEME_NAMES = {POS_SCHEME_PS: "PS", POS_SCHEME_SFB: "SFB", POS_SCHEME_ADAM: "ADAM"}
+
+
+class PoseidonError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        msg = lib().pos_last_error().decode(errors="replace")
+        super().__init__(f"{where} -> {code}: {msg}")
+        self.code = code
+
+
+def _chk(rc: int, where: str) -> int:
+    if rc < 0:
+        raise PoseidonError(rc, where)
+    return rc
+
+
+# ------------------------------------------------------------------ pure host functions ----
+def pos_version() -> int:
+    return lib().pos_version()
+
+
+def pos_choose_scheme(M: int, N: int, K: int, P: int) -> int:
+    return _chk(lib().pos_choose_scheme(M, N, K, P), "pos_choose_scheme")
+
+
+def pos_choose_scheme2(kind: int, M: int, N: int, K: int, P1: int, P2: int) -> int:
+    return _chk(lib().pos_choose_scheme2(kind, M, N, K, P1, P2), "pos_choose_scheme2")
+
+
+def pos_cost_elems(scheme: int, role: int, M: int, N: int, K: int, P1: int, P2: int):
+    """Table 1 cost as an exact (numerator, denominator) pair."""
+    num, den = C.c_uint64(), C.c_uint64()
+    _chk(lib().pos_cost_elems(scheme, role, M, N, K, P1, P2, C.byref(num), C.byref(den)),
+         "pos_cost_elems")
+    return num.value, den.value
+
+
+def pos_shard_stride(n: int, P: int) -> int:
+    return _chk(lib().pos_shard_stride(n, P), "pos_shard_stride")
+
+
+def pos_shard_range(n: int, P: int, r: int):
+    b, e = C.c_int64(), C.c_int64()
+    _chk(lib().pos_shard_range(n, P, r, C.byref(b), C.byref(e)), "pos_shard_range")
+    return b.value, e.value
+
+
+def pos_padded_size(n: int, P: int) -> int:
+    return _chk(lib().pos_padded_size(n, P), "pos_padded_size")
+
+
+def pos_factor_row_elems(M: int, N: int) -> int:
+    return _chk(lib().pos_factor_row_elems(M, N), "pos_factor_row_elems")
+
+
+# --------------------------------------------------------------------- torch marshalling ----
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _in_dtype(t):
+    import torch
+    if t.dtype == torch.bfloat16:
+        return POS_IN_BF16
+    if t.dtype == torch.float32:
+        return POS_IN_F32
+    raise TypeError(f"factors must be bf16 or fp32, got {t.dtype}")
+
+
+def _check_factors(u, v, W):
+    assert u.is_cuda and v.is_cuda and W.is_cuda, "tensors must live on the GPU"
+    assert u.is_contiguous() and v.is_contiguous() and W.is_contiguous()
+    assert u.dtype == v.dtype and W.dtype.is_floating_point and W.element_size() == 4
+    K, M = u.shape
+    K2, N = v.shape
+    assert K == K2 and (tuple(W.shape[-2:]) == (M, N) or W.numel() >= M * N)
+    return M, N, K
+
+
+def pos_pack_factors(u, v, slot, dtype: int, stream=None):
+    K, M = u.shape
+    N = v.shape[1]
+    _chk(lib().pos_pack_factors(M, N, K, _in_dtype(u), dtype, _ptr(u), _ptr(v), _ptr(slot),
+                                _stream(stream)), "pos_pack_factors")
+
+
+def pos_reconstruct_apply(M, N, KP, dtype, G, W, b=None, alpha=1.0, accumulate=True, ldw=None,
+                          stream=None):
+    _chk(lib().pos_reconstruct_apply(M, N, KP, dtype, _ptr(G), int(accumulate), _ptr(W),
+                                     N if ldw is None else ldw, _ptr(b), alpha, _stream(stream)),
+         "pos_reconstruct_apply")
+
+
+def pos_ps_apply(g, W, count, alpha, stream=None):
+    _chk(lib().pos_ps_apply(_ptr(g), _ptr(W), count, alpha, _stream(stream)), "pos_ps_apply")
+
+
+class Context:
+    """pos_ctx: NCCL communicator + comm stream + workspace, on the current CUDA device."""
+
+    def __init__(self, handle, world, rank, local):
+        self.h = handle
+        self.world, self.rank, self.local = world, rank, local
+
+    # construction ---------------------------------------------------------------------
+    @classmethod
+    def local_sim(cls, P: int = 1) -> "Context":
+        h = C.c_void_p()
+        _chk(lib().pos_init_local(P, C.byref(h)), "pos_init_local")
+        return cls(h, P, 0, True)
+
+    @classmethod
+    def from_unique_id(cls, uid: bytes, world: int, rank: int) -> "Context":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(uid, 128)
+        _chk(lib().pos_init(buf, world, rank, C.byref(h)), "pos_init")
+        return cls(h, world, rank, False)
+
+    @classmethod
+    def from_torch_distributed(cls, group=None) -> "Context":
+        """Rank 0 creates the NCCL unique id; torch.distributed broadcasts it (plumbing only)."""
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if world == 1:
+            return cls.from_unique_id(bytes(128), 1, 0)
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            _chk(lib().pos_get_unique_id(uid), "pos_get_unique_id")
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).to(dev)
+        dist.broadcast(t, src=0, group=group)
+        return cls.from_unique_id(bytes(t.cpu().tolist()), world, rank)
+
+    def close(self):
+        if self.h:
+            _chk(lib().pos_finalize(self.h), "pos_finalize")
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def async_error(self) -> int:
+        return lib().pos_get_async_error(self.h)
+
+    def set_max_ctas(self, n: int):
+        _chk(lib().pos_set_max_ctas(self.h, n), "pos_set_max_ctas")
+
+    # one-shot syncs ---------------------------------------------------------------------
+    def sync_layer_sfb(self, u, v, W, b=None, alpha=1.0, dtype="bf16", stream=None):
+        """pos_sync_layer_sfb: W += alpha * sum over all ranks' samples of u v^T (and b += alpha * sum u)."""
+        M, N, K = _check_factors(u, v, W)
+        _chk(lib().pos_sync_layer_sfb(self.h, M, N, K, _in_dtype(u), DTYPES[dtype], _ptr(u), _ptr(v),
+                                      _ptr(W), _ptr(b), alpha, _stream(stream)), "pos_sync_layer_sfb")
+
+    def sync_layer_ps(self, n, grad, W, alpha=1.0, stream=None):
+        """pos_sync_layer_ps: grad and W are flat fp32 buffers of >= pos_padded_size(n, P)."""
+        assert grad.numel() >= pos_padded_size(n, self.world) and W.numel() >= pos_padded_size(n, self.world)
+        _chk(lib().pos_sync_layer_ps(self.h, n, _ptr(grad), _ptr(W), alpha, _stream(stream)),
+             "pos_sync_layer_ps")
+
+    def sync_layer_fc_ps(self, u, v, grad, Wb, has_bias, alpha=1.0, dtype="bf16", stream=None):
+        K, M = u.shape
+        N = v.shape[1]
+        _chk(lib().pos_sync_layer_fc_ps(self.h, M, N, K, _in_dtype(u), DTYPES[dtype], _ptr(u), _ptr(v),
+                                        _ptr(grad), _ptr(Wb), int(has_bias), alpha, _stream(stream)),
+             "pos_sync_layer_fc_ps")
+
+    def sim_sync_layer_sfb(self, us, vs, W, b=None, alpha=1.0, dtype="bf16", stream=None):
+        assert self.local and len(us) == len(vs) == self.world
+        M, N, K = _check_factors(us[0], vs[0], W)
+        up = (C.c_void_p * len(us))(*[u.data_ptr() for u in us])
+        vpp = (C.c_void_p * len(vs))(*[v.data_ptr() for v in vs])
+        _chk(lib().pos_sim_sync_layer_sfb(self.h, M, N, K, _in_dtype(us[0]), DTYPES[dtype], up, vpp,
+                                          _ptr(W), _ptr(b), alpha, _stream(stream)),
+             "pos_sim_sync_layer_sfb")
+
+    def sim_sync_layer_ps(self, grads, W, alpha=1.0, n=None, stream=None):
+        assert self.local and len(grads) == self.world
+        n = W.numel() if n is None else n
+        gp = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        _chk(lib().pos_sim_sync_layer_ps(self.h, n, gp, _ptr(W), alpha, _stream(stream)),
+             "pos_sim_sync_layer_ps")
+
+
+class Scheduler:
+    """pos_sched: WFBP per-layer scheduler (Algorithm 2 on CUDA streams/events)."""
+
+    def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False):
+        self.ctx = ctx
+        h = C.c_void_p()
+        flags = (POS_SCHED_TIMING if timing else 0) | (POS_SCHED_SEQUENTIAL if sequential else 0)
+        _chk(lib().pos_sched_create(ctx.h, n_layers, flags, C.byref(h)), "pos_sched_create")
+        self.h = h
+        self.L = n_layers
+
+    def add_fc(self, l, M, N, K, W, b=None, grad=None, dtype="bf16", in_dtype=POS_IN_BF16, force_scheme=-1):
+        return _chk(lib().pos_sched_add_fc(self.h, l, M, N, K, in_dtype, DTYPES[dtype], _ptr(W), _ptr(b),
+                                           _ptr(grad), force_scheme), "pos_sched_add_fc")
+
+    def add_dense(self, l, n, W, grad):
+        return _chk(lib().pos_sched_add_dense(self.h, l, n, _ptr(W), _ptr(grad)), "pos_sched_add_dense")
+
+    def begin(self, alpha):
+        _chk(lib().pos_sched_begin(self.h, alpha), "pos_sched_begin")
+
+    def factors_ready(self, l, u, v, stream=None):
+        _chk(lib().pos_sched_factors_ready(self.h, l, _ptr(u), _ptr(v), _stream(stream)),
+             "pos_sched_factors_ready")
+
+    def grad_ready(self, l, stream=None):
+        _chk(lib().pos_sched_grad_ready(self.h, l, _stream(stream)), "pos_sched_grad_ready")
+
+    def wait_layer(self, l, stream=None):
+        _chk(lib().pos_sched_wait_layer(self.h, l, _stream(stream)), "pos_sched_wait_layer")
+
+    def end(self, stream=None):
+        _chk(lib().pos_sched_end(self.h, _stream(stream)), "pos_sched_end")
+
+    def scheme(self, l):
+        return _chk(lib().pos_sched_scheme(self.h, l), "pos_sched_scheme")
+
+    def timing(self, l):
+        a, b, c = C.c_float(), C.c_float(), C.c_float()
+        _chk(lib().pos_sched_timing(self.h, l, C.byref(a), C.byref(b), C.byref(c)), "pos_sched_timing")
+        return a.value, b.value, c.value
+
+    def close(self):
+        if self.h:
+            lib().pos_sched_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+__all__ = [n for n in dir() if n.startswith(("pos_", "POS_"))] + [
+    "Context", "Scheduler", "PoseidonError", "DTYPES", "SCHEME_NAMES", "LIB_PATH", "lib"]

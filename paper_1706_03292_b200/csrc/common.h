@@ -1,0 +1,76 @@
+// Internal helpers shared by the libposeidon translation units (never installed, never included
+// by anything outside csrc/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "poseidon.h"
+
+namespace pos {
+
+// thread-local last-error message (pos_last_error)
+void set_error(const char* fmt, ...);
+void clear_error();
+
+#define POS_FAIL(code, ...)          \
+  do {                               \
+    ::pos::set_error(__VA_ARGS__);   \
+    return (code);                   \
+  } while (0)
+
+#define POS_CHECK_ARG(cond, ...)                       \
+  do {                                                 \
+    if (!(cond)) POS_FAIL(POS_EINVAL, __VA_ARGS__);    \
+  } while (0)
+
+#define POS_CUDA_TRY(expr)                                                             \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      POS_FAIL(POS_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),      \
+               __FILE__, __LINE__);                                                    \
+  } while (0)
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// gathered factor row layout: [u (M_pad) | v (N_pad)], pads of 8 elements (16 B for bf16)
+inline int64_t m_pad(int64_t M) { return round_up(M, 8); }
+inline int64_t n_pad(int64_t N) { return round_up(N, 8); }
+inline int64_t row_elems(int64_t M, int64_t N) { return m_pad(M) + n_pad(N); }
+inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4; }
+
+int num_sms();
+
+// ---- kernel launchers (return cudaError_t of the launch) ----
+cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
+                                const void* u, const void* v, void* slot, cudaStream_t s);
+cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
+                               int32_t accumulate, float* b, float alpha, cudaStream_t s);
+cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s);
+constexpr int kMaxSimP = 16;
+cudaError_t launch_sim_ps_reduce_apply(const float* const* grads, int P, float* W, int64_t n,
+                                       float alpha, cudaStream_t s);
+// SIMT fp32 FFMA reconstruct-and-apply (POS_DT_F32, and the odd-ldw path)
+cudaError_t launch_sfb_simt(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
+                            int32_t accumulate, float* W, int64_t ldw, float alpha,
+                            cudaStream_t s);
+// tcgen05 / TMEM / TMA reconstruct-and-apply (POS_DT_BF16 / POS_DT_TF32). Returns
+// cudaErrorNotSupported if the shape/alignment cannot use TMA (caller falls back to SIMT).
+cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
+                          int32_t accumulate, float* W, int64_t ldw, float alpha, int max_ctas,
+                          cudaStream_t s);
+bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G);
+
+// A4 + A4b dispatcher used by the C ABI and the context code
+int reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
+                      int32_t accumulate, float* W, int64_t ldw, float* b, float alpha,
+                      int max_ctas, cudaStream_t s);
+
+}  // namespace pos

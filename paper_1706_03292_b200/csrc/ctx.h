@@ -1,0 +1,42 @@
+// Internal definition of the context (pos_ctx) shared by ctx.cpp and sched.cpp.
+#pragma once
+
+#include <nccl.h>
+
+#include "common.h"
+
+struct pos_ctx {
+  int world = 1;         // number of workers P (real ranks, or simulated for pos_init_local)
+  int rank = 0;
+  int device = 0;
+  bool local = false;    // pos_init_local: simulated P, no NCCL
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;  // high-priority stream for collectives (scheduler)
+  int max_ctas = 0;
+  void* ws = nullptr;    // one-shot workspace (grow-only)
+  size_t ws_bytes = 0;
+  int sticky = POS_OK;   // first asynchronous error seen
+};
+
+namespace pos {
+
+// grow-only workspace; synchronises the device when it has to reallocate
+int ctx_workspace(pos_ctx* c, size_t bytes, void** out);
+// record a CUDA / NCCL failure as sticky and format the message
+int ctx_cuda_fail(pos_ctx* c, cudaError_t e, const char* what);
+int ctx_nccl_fail(pos_ctx* c, ncclResult_t r, const char* what);
+// polls the communicator for asynchronous errors (sticky)
+int ctx_check(pos_ctx* c);
+
+inline ncclDataType_t nccl_type(int32_t dtype) {
+  return dtype == POS_DT_BF16 ? ncclBfloat16 : ncclFloat32;
+}
+
+// stages shared by the one-shot entry points and the scheduler
+int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
+                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done);
+int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
+                        int32_t dtype, const void* u, const void* v, void* pack_buf, float* grad,
+                        int32_t has_bias, cudaStream_t s);
+
+}  // namespace pos

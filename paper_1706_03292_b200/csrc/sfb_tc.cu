@@ -1,0 +1,448 @@
+// A4 — SFB reconstruct-and-apply on the 5th-generation tensor cores (sm_100a).
+//
+//   W[m][n] = (accumulate ? W[m][n] : 0) + alpha * sum_{j < KP} U[j][m] * V[j][n]
+//
+// PAPER:111 §2.1: the FC gradient of one sample is u v^T, and SFB "reconstruct[s] the gradient
+// matrices using u, v locally"; Eq. 2 sums the P workers' batches. With the K*P
+// gathered factor rows stacked as U (KP x M) and V (KP x N) that is the dense contraction
+// U^T V with inner dimension KP, fused here with the SGD apply of PAPER:107 ("apply (+)").
+//
+// Design:
+//  * persistent, warp-specialised CTA, one per SM; 128 x 256 output tile; tiles in static
+//    round-robin order (deterministic, no split-K, no atomics -> bitwise-identical replicas);
+//  * operands U, V streamed by TMA (128-byte swizzle, MN-major: m / n is the contiguous
+//    direction of the gathered rows) into a 3-stage smem ring, consumed by tcgen05.mma issued by
+//    one thread, accumulating in TMEM (fp32). Two 256-column TMEM accumulators: the epilogue of
+//    tile i overlaps the MMAs of tile i+1;
+//  * the W tile (the HBM-dominant traffic: 8 bytes per element) is streamed in 128 x 32 fp32
+//    sub-tiles by a second TMA producer warp into a 4-slot ring, updated in shared memory by the
+//    4 epilogue warps (tcgen05.ld 32x32b -> fma -> st.shared) and written back by TMA store.
+//
+// Warp roles (256 threads): w0 operand TMA producer, w1 MMA issuer + TMEM owner, w2 W TMA
+// producer, w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes 32*(w%4) .. +31 = tile rows).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.h"
+
+namespace pos {
+namespace {
+
+constexpr int BM = 128;             // tile rows (m) = UMMA M = TMEM lanes
+constexpr int BN = 256;             // tile cols (n) = UMMA N = TMEM columns per accumulator
+constexpr int STAGES = 3;           // operand ring depth
+constexpr int WSLOTS = 4;           // W sub-tile ring depth
+constexpr int WSUB = 32;            // W sub-tile columns (32 fp32 = one 128-byte swizzle row)
+constexpr int NSUB = BN / WSUB;     // sub-tiles per tile
+constexpr int SWZ = 128;            // swizzle span in bytes (one operand "row" chunk)
+constexpr int A_BYTES = SWZ * BM;   // per stage: BK rows x BM elements = 128 B x BM (any dtype)
+constexpr int B_BYTES = SWZ * BN;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int W_BYTES = BM * WSUB * 4;
+constexpr int SMEM_DATA = STAGES * STAGE_BYTES + WSLOTS * W_BYTES;
+constexpr int SMEM_BARS = 8 * (2 * STAGES + 2 * WSLOTS + 4) + 16;
+constexpr int SMEM_TOTAL = SMEM_DATA + SMEM_BARS + 1024;   // + alignment slack
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 2 * BN;
+
+static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+
+// ------------------------------------------------------------------------------------ PTX ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t bar, uint32_t dst,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(map), "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, one elected thread issues for the whole CTA.
+template <bool kTF32>
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+// mbarrier arrives when all previously issued tcgen05 ops of this thread have completed
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100). For MN-major operands the
+// leading byte offset (LBO) is the distance between 128-byte chunks along M/N and the stride
+// byte offset (SBO) the distance between 8-row groups along K.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // layout: SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: fp32 accumulate, A/B format (BF16 = 1, TF32 = 2), both MN-major,
+// N = BN, M = BM.
+template <bool kTF32>
+__host__ __device__ constexpr uint32_t instr_desc() {
+  return (1u << 4) | ((kTF32 ? 2u : 1u) << 7) | ((kTF32 ? 2u : 1u) << 10) | (1u << 15) |
+         (1u << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// number of W sub-tiles of the tile starting at column n0 that intersect [0, N)
+__device__ __forceinline__ int nsub_of(int64_t N, int n0) {
+  const int64_t s = (N - n0 + WSUB - 1) / WSUB;
+  return s < NSUB ? (int)s : NSUB;
+}
+
+struct TileInfo {
+  int64_t M, N, KP;
+  int nb_n;        // tiles along n
+  int num_tiles;
+  int nkb;         // k blocks
+};
+
+template <bool kTF32>
+__global__ void __launch_bounds__(THREADS, 1)
+sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmW, TileInfo ti, float alpha, int accumulate) {
+  constexpr int EB = kTF32 ? 4 : 2;          // element bytes
+  constexpr int BK = SWZ / EB;               // k rows per stage (64 bf16 / 32 tf32)
+  constexpr int CHUNK = SWZ / EB;            // elements per 128-byte chunk along m / n
+  constexpr int UK = 32 / EB;                // UMMA K (16 bf16 / 8 tf32)
+  constexpr int BOX_BYTES = BK * SWZ;        // one TMA box: BK rows x 128 B
+  constexpr uint32_t IDESC = instr_desc<kTF32>();
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sW0 = sbase + STAGES * STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_DATA);
+  const uint32_t b_full = smem_u32(bars), b_empty = b_full + 8 * STAGES;
+  const uint32_t b_wfull = b_empty + 8 * STAGES, b_wempty = b_wfull + 8 * WSLOTS;
+  const uint32_t b_tfull = b_wempty + 8 * WSLOTS, b_tempty = b_tfull + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * WSLOTS + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, 1); }
+    for (int i = 0; i < WSLOTS; ++i) { mbar_init(b_wfull + 8 * i, 1); mbar_init(b_wempty + 8 * i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(b_tfull + 8 * i, 1); mbar_init(b_tempty + 8 * i, 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== operand TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+        const int m0 = (t / ti.nb_n) * BM, n0 = (t % ti.nb_n) * BN;
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          mbar_wait(b_empty + 8 * stage, phase ^ 1);
+          const uint32_t full = b_full + 8 * stage;
+          mbar_expect_tx(full, STAGE_BYTES);
+          const uint32_t sA = sbase + stage * STAGE_BYTES, sB = sA + A_BYTES;
+          const int k0 = kb * BK;
+#pragma unroll
+          for (int c = 0; c < BM / CHUNK; ++c) tma_load_2d(&tmA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
+#pragma unroll
+          for (int c = 0; c < BN / CHUNK; ++c) tma_load_2d(&tmB, full, sB + c * BOX_BYTES, n0 + c * CHUNK, k0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (single thread) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+        mbar_wait(b_tempty + 8 * acc, aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < ti.nkb; ++kb) {
+          mbar_wait(b_full + 8 * stage, phase);
+          tc_fence_after();
+          const uint32_t sA = sbase + stage * STAGE_BYTES, sB = sA + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t ad = smem_desc(sA + kk * UK * SWZ, BOX_BYTES, 8 * SWZ);
+            const uint64_t bd = smem_desc(sB + kk * UK * SWZ, BOX_BYTES, 8 * SWZ);
+            umma<kTF32>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+          }
+          umma_commit(b_empty + 8 * stage);   // frees the smem stage when these MMAs finish
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(b_tfull + 8 * acc);        // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else if (warp == 2) {
+    // ===================== W sub-tile TMA producer =====================
+    if (lane == 0) {
+      int ws = 0;
+      uint32_t wphase = 0;
+      for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+        const int m0 = (t / ti.nb_n) * BM, n0 = (t % ti.nb_n) * BN;
+        const int nsub = nsub_of(ti.N, n0);
+        for (int j = 0; j < nsub; ++j) {
+          mbar_wait(b_wempty + 8 * ws, wphase ^ 1);
+          const uint32_t wf = b_wfull + 8 * ws;
+          if (accumulate) {
+            mbar_expect_tx(wf, W_BYTES);
+            tma_load_2d(&tmW, wf, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
+          } else {
+            mbar_arrive(wf);
+          }
+          if (++ws == WSLOTS) { ws = 0; wphase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> regs, W += alpha * acc in smem, TMA store ========
+    const int et = threadIdx.x - 128;         // tile row owned by this thread
+    const int q = warp & 3;                   // TMEM lane quadrant of this warp
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int acc = 0;
+    uint32_t aphase = 0;
+    int ws = 0;
+    uint32_t wphase = 0;
+    int pending = -1;                         // slot whose TMA store has not been retired yet
+    for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+      const int m0 = (t / ti.nb_n) * BM, n0 = (t % ti.nb_n) * BN;
+      const int nsub = nsub_of(ti.N, n0);
+      mbar_wait(b_tfull + 8 * acc, aphase);
+      tc_fence_after();
+      for (int j = 0; j < nsub; ++j) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + lane_addr + acc * BN + j * WSUB, r);
+        if (j == nsub - 1) {                  // accumulator fully drained by this thread
+          tc_fence_before();
+          mbar_arrive(b_tempty + 8 * acc);
+        }
+        mbar_wait(b_wfull + 8 * ws, wphase);
+        const uint32_t row = sW0 + ws * W_BYTES + et * SWZ;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t a = row + ((uint32_t)(c ^ (et & 7)) << 4);   // 128-byte swizzle
+          float4 w;
+          if (accumulate) {
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(w.x), "=f"(w.y), "=f"(w.z), "=f"(w.w) : "r"(a));
+          } else {
+            w = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          w.x = fmaf(alpha, __uint_as_float(r[4 * c + 0]), w.x);
+          w.y = fmaf(alpha, __uint_as_float(r[4 * c + 1]), w.y);
+          w.z = fmaf(alpha, __uint_as_float(r[4 * c + 2]), w.z);
+          w.w = fmaf(alpha, __uint_as_float(r[4 * c + 3]), w.w);
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(w.x), "f"(w.y),
+                       "f"(w.z), "f"(w.w)
+                       : "memory");
+        }
+        fence_proxy_async_smem();             // generic-proxy smem writes -> visible to TMA
+        named_bar_sync(1, 128);
+        if (et == 0) {
+          tma_store_2d(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
+          bulk_commit();
+          if (pending >= 0) {
+            bulk_wait_read<1>();              // the previous store has finished reading smem
+            mbar_arrive(b_wempty + 8 * pending);
+          }
+          pending = ws;
+        }
+        if (++ws == WSLOTS) { ws = 0; wphase ^= 1; }
+      }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (et == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------------ host side ----------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool kTF32>
+cudaError_t launch_impl(int64_t M, int64_t N, int64_t KP, const void* G, int32_t accumulate,
+                        float* W, int64_t ldw, float alpha, int max_ctas, cudaStream_t s) {
+  constexpr int EB = kTF32 ? 4 : 2;
+  constexpr int BK = SWZ / EB, CHUNK = SWZ / EB;
+  const int64_t R = row_elems(M, N), Mp = m_pad(M);
+  const CUtensorMapDataType dt =
+      kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUtensorMap tmA, tmB, tmW;
+  const uint8_t* g = static_cast<const uint8_t*>(G);
+  if (!encode_2d(&tmA, dt, g, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK) ||
+      !encode_2d(&tmB, dt, g + Mp * EB, (uint64_t)N, (uint64_t)KP, (uint64_t)(R * EB), CHUNK,
+                 BK) ||
+      !encode_2d(&tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, W, (uint64_t)N, (uint64_t)M,
+                 (uint64_t)(ldw * 4), WSUB, BM))
+    return cudaErrorInvalidValue;
+  TileInfo ti;
+  ti.M = M; ti.N = N; ti.KP = KP;
+  ti.nb_n = (int)((N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)ti.nb_n * ((M + BM - 1) / BM);
+  if (tiles > INT32_MAX) return cudaErrorInvalidValue;
+  ti.num_tiles = (int)tiles;
+  ti.nkb = (int)((KP + BK - 1) / BK);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (grid > ti.num_tiles) grid = ti.num_tiles;
+  sfb_tc_kernel<kTF32><<<grid, THREADS, SMEM_TOTAL, s>>>(tmA, tmB, tmW, ti, alpha, accumulate);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
+  return (ldw % 4) == 0 && aligned16(W) && aligned16(G) && N >= 1 && get_encode() != nullptr;
+}
+
+cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
+                          int32_t accumulate, float* W, int64_t ldw, float alpha, int max_ctas,
+                          cudaStream_t s) {
+  if (dtype == POS_DT_TF32)
+    return launch_impl<true>(M, N, KP, G, accumulate, W, ldw, alpha, max_ctas, s);
+  return launch_impl<false>(M, N, KP, G, accumulate, W, ldw, alpha, max_ctas, s);
+}
+
+}  // namespace pos

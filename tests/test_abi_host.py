@@ -1,0 +1,117 @@
+"""C-ABI library (CPU-only checks): it loads, exports every symbol include/poseidon.h declares,
+and its pure host functions agree with the oracle BIT-EXACTLY (scheme choice, Table 1 costs,
+shard table). No compute calls (no GPU here)."""
+import re
+from fractions import Fraction
+
+import pytest
+
+import paper_1706_03292_b200 as pos
+from oracle import cost, shard
+
+HEADER = __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "include", "poseidon.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pos_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_functions()
+    assert len(names) >= 30
+    lib = pos.lib()
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    # the binding declares exactly the header's functions (same names)
+    from paper_1706_03292_b200._lib import SIGNATURES
+    assert sorted(SIGNATURES) == names
+
+
+def test_version():
+    assert pos.pos_version() == 100
+
+
+def test_choose_scheme_tiny_grid_bit_exact():
+    """Every (M,N,K,P) in M,N in [1,32], K in [1,16], P in [1,16] (262,144 cases) vs Alg. 1 oracle."""
+    lib = pos.lib()
+    mismatches = 0
+    n_sfb = 0
+    for M in range(1, 33):
+        for N in range(1, 33):
+            for K in range(1, 17):
+                for P in range(1, 17):
+                    got = lib.pos_choose_scheme(M, N, K, P)
+                    exp = cost.SFB if 2 * K * (P - 1) * (M + N) * P <= 2 * M * N * (2 * P - 2) else cost.PS
+                    n_sfb += got == pos.POS_SCHEME_SFB
+                    mismatches += (got == pos.POS_SCHEME_SFB) != (exp == cost.SFB)
+    assert mismatches == 0
+    assert n_sfb == 42300
+
+
+def test_choose_scheme_matches_oracle_fraction_form():
+    lib = pos.lib()
+    for M in range(1, 13):
+        for N in range(1, 13):
+            for K in range(1, 7):
+                for P1 in range(1, 7):
+                    for P2 in range(1, 7):
+                        for kind in (pos.POS_KIND_FC, pos.POS_KIND_DENSE):
+                            got = lib.pos_choose_scheme2(kind, M, N, K, P1, P2)
+                            exp = cost.best_scheme(cost.FC if kind == pos.POS_KIND_FC else cost.DENSE,
+                                                   M, N, K, P1, P2)
+                            assert pos.SCHEME_NAMES[got] == exp, (kind, M, N, K, P1, P2)
+    # the ceil() trap of reading S4
+    assert pos.pos_choose_scheme2(pos.POS_KIND_FC, 2, 9, 1, 3, 5) == pos.POS_SCHEME_PS
+
+
+def test_choose_scheme_large_shapes():
+    for (M, N, K, P) in [(4096, 4096, 32, 8), (1000, 1024, 128, 16), (21841, 4096, 32, 8),
+                         (4096, 25088, 32, 8), (4096, 4096, 128, 32), (4096, 4096, 129, 32),
+                         (1 << 30, 1 << 30, 1 << 30, 1 << 20)]:
+        got = pos.SCHEME_NAMES[pos.pos_choose_scheme(M, N, K, P)]
+        assert got == cost.best_scheme_p(cost.FC, M, N, K, P), (M, N, K, P)
+
+
+@pytest.mark.parametrize("scheme,role", [(pos.POS_SCHEME_PS, r) for r in range(3)] +
+                         [(pos.POS_SCHEME_SFB, pos.POS_ROLE_WORKER)] +
+                         [(pos.POS_SCHEME_ADAM, r) for r in range(3)])
+def test_cost_elems_exact(scheme, role):
+    names = {pos.POS_SCHEME_PS: cost.PS, pos.POS_SCHEME_SFB: cost.SFB, pos.POS_SCHEME_ADAM: cost.ADAM}
+    roles = {0: cost.SERVER, 1: cost.WORKER, 2: cost.BOTH}
+    for (M, N, K, P1, P2) in [(4096, 4096, 32, 8, 8), (2, 9, 1, 3, 5), (1, 1, 1, 1, 1), (7, 3, 5, 4, 6),
+                              (21841, 4096, 32, 8, 8), (1000, 1024, 128, 16, 16)]:
+        num, den = pos.pos_cost_elems(scheme, role, M, N, K, P1, P2)
+        assert Fraction(num, den) == cost.cost(names[scheme], roles[role], M, N, K, P1, P2)
+
+
+def test_cost_elems_na_and_errors():
+    with pytest.raises(pos.PoseidonError) as e:
+        pos.pos_cost_elems(pos.POS_SCHEME_SFB, pos.POS_ROLE_SERVER, 4, 4, 1, 2, 2)
+    assert e.value.code == pos.POS_EUNSUPPORTED
+    with pytest.raises(pos.PoseidonError) as e:
+        pos.pos_choose_scheme(0, 4, 1, 2)
+    assert e.value.code == pos.POS_EINVAL and "must be >= 1" in str(e.value)
+
+
+def test_shard_table_bit_exact():
+    lib = pos.lib()
+    import ctypes as C
+    b, e = C.c_int64(), C.c_int64()
+    for P in range(1, 9):
+        for n in range(1, 10001):
+            S = lib.pos_shard_stride(n, P)
+            assert S == shard.shard_stride(n, P)
+            assert lib.pos_padded_size(n, P) == P * S
+            for r in range(P):
+                assert lib.pos_shard_range(n, P, r, C.byref(b), C.byref(e)) == 0
+                assert (b.value, e.value) == shard.shard_range(n, P, r)
+    assert lib.pos_shard_stride(0, 4) < 0
+    assert lib.pos_shard_range(10, 2, 2, C.byref(b), C.byref(e)) == pos.POS_EINVAL
+
+
+def test_factor_row_layout():
+    assert pos.pos_factor_row_elems(21841, 4096) == 21848 + 4096
+    assert pos.pos_factor_row_elems(1, 1) == 16
+    assert pos.pos_factor_row_elems(64, 64) == 128

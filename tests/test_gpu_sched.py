@@ -1,0 +1,184 @@
+"""WFBP scheduler on one GPU (world-1 context): results vs oracle, WFBP == sequential bitwise
+(SPEC:369), hazards (WAR on W vs the backward's grad_input read, RAW for the next forward;
+PAPER:152), and state-machine misuse -> POS_ESTATE."""
+import numpy as np
+import pytest
+
+import synth_inputs as si
+from oracle import sync
+from tests._util import have_gpu, to_dev, to_host
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a CUDA GPU")]
+
+if have_gpu():
+    import torch
+    import paper_1706_03292_b200 as pos
+
+# forward-order layer list: (kind, dims, force_scheme)
+LAYERS = [("dense", 1728 + 64, None), ("dense", 2359808, None), ("fc", (4096, 25088, 32), None),
+          ("fc", (1000, 4100, 32), pos.POS_SCHEME_PS if have_gpu() else None), ("fc", (21841, 4096, 32), None)]
+
+
+def make_model(seed):
+    """Host arrays: per layer W (+b), the trigger inputs (factors or grad)."""
+    out = []
+    for l, (kind, dims, force) in enumerate(LAYERS):
+        g = si.rng(seed, l)
+        if kind == "dense":
+            n = dims
+            out.append({"kind": kind, "n": n, "W": si.exact_weights(g, n), "g": si.exact_dense_grad(g, n)})
+        else:
+            M, N, K = dims
+            u, v = si.exact_factors(g, K, M, N)
+            out.append({"kind": kind, "M": M, "N": N, "K": K, "W": si.exact_weights(g, M, N),
+                        "b": si.exact_weights(g, M), "u": u, "v": v, "force": force})
+    return out
+
+
+def oracle_result(model, alpha):
+    res = []
+    for d in model:
+        if d["kind"] == "dense":
+            res.append((sync.ps_update(d["W"], [d["g"]], alpha), None))
+        else:
+            res.append(sync.sfb_update(d["W"], d["b"], [d["u"]], [d["v"]], alpha))
+    return res
+
+
+def run(model, alpha, sequential=False, timing=False, delay_cycles=0):
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, len(model), timing=timing, sequential=sequential)
+    dev = []
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            n = d["n"]
+            P = pos.pos_padded_size(n, 1)
+            W = torch.zeros(P, device="cuda"); W[:n] = to_dev(d["W"])
+            G = torch.zeros(P, device="cuda"); G[:n] = to_dev(d["g"])
+            assert sch.add_dense(l, n, W, G) == pos.POS_SCHEME_PS
+            dev.append({"W": W, "G": G})
+        else:
+            M, N, K = d["M"], d["N"], d["K"]
+            if d["force"] == pos.POS_SCHEME_PS:
+                n = M * N + M
+                P = pos.pos_padded_size(n, 1)
+                flat = torch.zeros(P, device="cuda")
+                flat[:M * N] = to_dev(d["W"]).reshape(-1)
+                flat[M * N:n] = to_dev(d["b"])
+                W, b = flat[:M * N].view(M, N), flat[M * N:n]
+                grad = torch.empty(P, device="cuda")
+                s = sch.add_fc(l, M, N, K, W, b, grad, dtype="bf16", in_dtype=pos.POS_IN_BF16, force_scheme=pos.POS_SCHEME_PS)
+                assert s == pos.POS_SCHEME_PS
+            else:
+                W, b, grad = to_dev(d["W"]), to_dev(d["b"]), None
+                s = sch.add_fc(l, M, N, K, W, b, None, dtype="bf16", in_dtype=pos.POS_IN_BF16)
+                assert s == pos.POS_SCHEME_SFB  # Alg. 1 at P = 1
+            dev.append({"W": W, "b": b, "grad": grad, "u": to_dev(d["u"], "bf16"), "v": to_dev(d["v"], "bf16")})
+    for l in range(len(model)):
+        assert sch.scheme(l) == (pos.POS_SCHEME_PS if model[l]["kind"] == "dense" or model[l].get("force") == pos.POS_SCHEME_PS else pos.POS_SCHEME_SFB)
+    producer = torch.cuda.Stream()
+    consumer = torch.cuda.current_stream()
+    producer.wait_stream(consumer)
+    gi = {}
+    sch.begin(alpha)
+    with torch.cuda.stream(producer):
+        for l in reversed(range(len(model))):            # backward order L..1
+            if model[l]["kind"] == "dense":
+                sch.grad_ready(l, producer)
+            else:
+                if delay_cycles:
+                    torch.cuda._sleep(delay_cycles)       # a slow b^l
+                # b^l reads W: grad_input = grad_output @ W (the WAR hazard the trigger must respect)
+                gi[l] = (dev[l]["u"].float() @ dev[l]["W"].float()) if delay_cycles else None
+                sch.factors_ready(l, dev[l]["u"], dev[l]["v"], producer)
+    sch.end(consumer)
+    torch.cuda.synchronize()
+    timings = [sch.timing(l) for l in range(len(model))] if timing else None
+    out = []
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            out.append((to_host(dev[l]["W"][:d["n"]]), None))
+        else:
+            out.append((to_host(dev[l]["W"]), to_host(dev[l]["b"])))
+    sch.close()
+    ctx.close()
+    return out, timings, gi
+
+
+def test_sched_wfbp_matches_oracle_and_sequential_bitwise():
+    model = make_model(1)
+    a = si.EXACT_ALPHA
+    ref = oracle_result(model, a)
+    wfbp, _, _ = run(model, a)
+    seq, _, _ = run(model, a, sequential=True)
+    for (Wr, br), (Ww, bw), (Ws, bs) in zip(ref, wfbp, seq):
+        assert np.array_equal(Ww, Wr)
+        assert np.array_equal(Ws, Ww)
+        if br is not None:
+            assert np.array_equal(bw, br) and np.array_equal(bs, bw)
+
+
+def test_sched_timing_reports():
+    model = make_model(2)
+    _, t, _ = run(model, si.EXACT_ALPHA, timing=True)
+    for pack, comm, apply in t:
+        assert pack >= 0 and comm >= 0 and apply > 0
+
+
+def test_sched_war_hazard_with_slow_backward():
+    """A slow b^l (device sleep) precedes the grad_input read of W; the sync of layer l must not
+    touch W before that read (i^l may update only once b^l has finished)."""
+    model = make_model(3)
+    a = si.EXACT_ALPHA
+    out, _, gi = run(model, a, delay_cycles=20_000_000)
+    ref = oracle_result(model, a)
+    for l, d in enumerate(model):
+        assert np.array_equal(out[l][0], ref[l][0])
+        if d["kind"] == "fc":
+            exp = d["u"].astype(np.float64) @ d["W"].astype(np.float64)   # must see the OLD W
+            assert np.array_equal(gi[l].cpu().numpy().astype(np.float64), exp)
+
+
+def test_sched_misuse_is_estate():
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, 2)
+    W = torch.zeros(pos.pos_padded_size(100, 1), device="cuda")
+    G = torch.zeros_like(W)
+    sch.add_dense(0, 100, W, G)
+    with pytest.raises(pos.PoseidonError) as e:
+        sch.begin(1.0)                        # layer 1 never added
+    assert e.value.code == pos.POS_ESTATE
+    sch.add_dense(1, 100, W.clone(), G.clone())
+    with pytest.raises(pos.PoseidonError) as e:
+        sch.add_dense(1, 100, W, G)           # added twice
+    assert e.value.code == pos.POS_ESTATE
+    sch.begin(1.0)
+    sch.grad_ready(1)
+    with pytest.raises(pos.PoseidonError) as e:
+        sch.grad_ready(1)                     # triggered twice
+    assert e.value.code == pos.POS_ESTATE
+    with pytest.raises(pos.PoseidonError) as e:
+        sch.end()                             # layer 0 not triggered
+    assert e.value.code == pos.POS_ESTATE
+    sch.grad_ready(0)
+    sch.end()
+    with pytest.raises(pos.PoseidonError) as e:
+        sch.factors_ready(0, W, W)            # not an FC layer
+    assert e.value.code == pos.POS_ESTATE
+    torch.cuda.synchronize()
+    sch.close()
+    ctx.close()
+
+
+def test_input_validation():
+    ctx = pos.Context.local_sim(2)
+    W = torch.zeros(64, 64, device="cuda")
+    with pytest.raises(pos.PoseidonError) as e:
+        pos.lib()  # noqa
+        ctx.sync_layer_sfb(torch.zeros(8, 64, device="cuda"), torch.zeros(8, 64, device="cuda"), W)
+    assert e.value.code == pos.POS_EINVAL and "pos_sim_sync_layer_sfb" in str(e.value)
+    g = torch.zeros(200, device="cuda")
+    with pytest.raises(pos.PoseidonError) as e:
+        c1 = pos.Context.from_unique_id(bytes(128), 1, 0)
+        c1.sync_layer_ps(100, g[1:], g[1:])   # misaligned
+    assert e.value.code == pos.POS_EINVAL
