@@ -215,9 +215,12 @@ int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer);
 int pos_sched_end(pos_sched* s, void* consumer);
 /* Query: the scheme chosen for layer l. */
 int pos_sched_scheme(pos_sched* s, int32_t l);
-/* With POS_SCHED_TIMING: device milliseconds of the last iteration's pack, collective(s) and
- * apply stages of layer l (synchronises on the layer's completion). */
+/* With POS_SCHED_TIMING: AVERAGE device milliseconds, over every iteration since the last reset,
+ * of layer l's pack, collective(s) (all-gather; or reduce-scatter + all-gather) and apply
+ * (reconstruct-and-apply; or shard apply) stages, each bracketed by CUDA events on the stream that
+ * runs it. Synchronises on the layer's outstanding iterations. Returns the iteration count (> 0). */
 int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, float* apply_ms);
+int pos_sched_timing_reset(pos_sched* s);
 int pos_sched_destroy(pos_sched* s);
 
 #ifdef __cplusplus

@@ -258,6 +258,9 @@ class Scheduler:
         _chk(lib().pos_sched_timing(self.h, l, C.byref(a), C.byref(b), C.byref(c)), "pos_sched_timing")
         return a.value, b.value, c.value
 
+    def timing_reset(self):
+        _chk(lib().pos_sched_timing_reset(self.h), "pos_sched_timing_reset")
+
     def close(self):
         if self.h:
             lib().pos_sched_destroy(self.h)

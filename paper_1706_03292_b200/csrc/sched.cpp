@@ -22,6 +22,13 @@
 namespace {
 
 constexpr int kPool = 4;
+constexpr int kTRing = 4;   // timing event sets per layer (iterations in flight)
+
+struct TSlot {
+  cudaEvent_t start = nullptr, packed = nullptr, gathered = nullptr, a0 = nullptr, a1 = nullptr,
+              done = nullptr;
+  bool used = false;
+};
 
 struct Layer {
   bool added = false;
@@ -34,7 +41,9 @@ struct Layer {
   float* grad = nullptr;
   void* gbuf = nullptr;   // SFB: P*K rows of the gathered factors; FC-on-PS: K rows (local)
   cudaEvent_t ev_ready = nullptr, ev_gathered = nullptr, ev_done = nullptr;
-  cudaEvent_t t_start = nullptr, t_packed = nullptr, t_apply0 = nullptr, t_apply1 = nullptr;
+  TSlot ring[kTRing];
+  double acc_pack = 0, acc_comm = 0, acc_apply = 0;
+  int64_t n_acc = 0;
   bool triggered = false;
   const void* u = nullptr;
   const void* v = nullptr;
@@ -54,6 +63,7 @@ struct pos_sched {
   int n_triggered = 0;
   std::vector<int> order;  // trigger order of the current iteration
   cudaEvent_t ev_end = nullptr;
+  int64_t iter = 0;        // iterations begun
 };
 
 using namespace pos;
@@ -67,6 +77,29 @@ int make_event(cudaEvent_t* e, bool timed) {
   return POS_OK;
 }
 
+// Fold a finished iteration's timing events into the layer's running sums.
+int harvest(Layer& ly, TSlot& t) {
+  if (!t.used) return POS_OK;
+  POS_CUDA_TRY(cudaEventSynchronize(t.done));
+  float pack = 0, comm = 0, apply = 0, extra = 0;
+  POS_CUDA_TRY(cudaEventElapsedTime(&pack, t.start, t.packed));
+  if (ly.scheme == POS_SCHEME_SFB) {
+    POS_CUDA_TRY(cudaEventElapsedTime(&comm, t.packed, t.gathered));   // all-gather
+    POS_CUDA_TRY(cudaEventElapsedTime(&apply, t.a0, t.a1));            // reconstruct-and-apply
+  } else {
+    POS_CUDA_TRY(cudaEventElapsedTime(&comm, t.packed, t.a0));         // reduce-scatter
+    POS_CUDA_TRY(cudaEventElapsedTime(&apply, t.a0, t.a1));            // shard apply
+    POS_CUDA_TRY(cudaEventElapsedTime(&extra, t.a1, t.done));          // all-gather
+    comm += extra;
+  }
+  ly.acc_pack += pack;
+  ly.acc_comm += comm;
+  ly.acc_apply += apply;
+  ly.n_acc += 1;
+  t.used = false;
+  return POS_OK;
+}
+
 // Enqueue sync(l) behind ly.ev_ready.
 int issue_layer(pos_sched* s, int l) {
   pos_ctx* c = s->ctx;
@@ -74,9 +107,16 @@ int issue_layer(pos_sched* s, int l) {
   cudaStream_t cs = c->comm_stream;
   const bool tm = timing(s);
   const int P = c->world;
+  TSlot* ts = nullptr;
+  if (tm) {
+    ts = &ly.ring[(s->iter - 1) % kTRing];
+    int rc0 = harvest(ly, *ts);
+    if (rc0) return rc0;
+    ts->used = true;
+  }
   POS_CUDA_TRY(cudaStreamWaitEvent(cs, ly.ev_ready, 0));
   if (s->flags & POS_SCHED_SEQUENTIAL) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_end, 0));
-  if (tm) POS_CUDA_TRY(cudaEventRecord(ly.t_start, cs));
+  if (tm) POS_CUDA_TRY(cudaEventRecord(ts->start, cs));
   int rc = POS_OK;
   if (ly.scheme == POS_SCHEME_SFB) {
     const int64_t R = row_elems(ly.M, ly.N), slot = ly.K * R;
@@ -86,22 +126,24 @@ int issue_layer(pos_sched* s, int l) {
     cudaError_t e = launch_pack_factors(ly.M, ly.N, ly.K, ly.in_dtype, ly.dtype, ly.u, ly.v,
                                         my_slot, cs);
     if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack launch");
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ly.t_packed, cs));
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->packed, cs));
     // Send + Receive: A3 all-gather of the factors
     if (P > 1) {
       ncclResult_t r = ncclAllGather(my_slot, ly.gbuf, (size_t)slot, nccl_type(ly.dtype), c->comm, cs);
       if (r != ncclSuccess) return ctx_nccl_fail(c, r, "ncclAllGather(factors)");
     }
     POS_CUDA_TRY(cudaEventRecord(ly.ev_gathered, cs));
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->gathered, cs));
     // Move(CPU2GPU) analogue: A4 + A4b on an apply stream
     cudaStream_t as = s->pool[l % kPool];
     POS_CUDA_TRY(cudaStreamWaitEvent(as, ly.ev_gathered, 0));
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ly.t_apply0, as));
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->a0, as));
     rc = reconstruct_apply(ly.M, ly.N, ly.K * P, ly.dtype, ly.gbuf, 1, ly.W, ly.N, ly.b, s->alpha,
                            c->max_ctas, as);
     if (rc != POS_OK) { if (c->sticky == POS_OK) c->sticky = rc; return rc; }
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ly.t_apply1, as));
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->a1, as));
     POS_CUDA_TRY(cudaEventRecord(ly.ev_done, as));
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->done, as));
   } else {
     int64_t n = ly.n;
     if (ly.kind == POS_KIND_FC) {
@@ -110,11 +152,12 @@ int issue_layer(pos_sched* s, int l) {
                                ly.grad, ly.b != nullptr, cs);
       if (rc != POS_OK) return rc;
     }
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ly.t_packed, cs));
-    rc = stage_ps_dense(c, n, ly.grad, ly.W, s->alpha, cs, tm ? ly.t_apply0 : nullptr,
-                        tm ? ly.t_apply1 : nullptr);
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->packed, cs));
+    rc = stage_ps_dense(c, n, ly.grad, ly.W, s->alpha, cs, tm ? ts->a0 : nullptr,
+                        tm ? ts->a1 : nullptr);
     if (rc != POS_OK) return rc;
     POS_CUDA_TRY(cudaEventRecord(ly.ev_done, cs));
+    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->done, cs));
   }
   return POS_OK;
 }
@@ -173,12 +216,15 @@ static int add_common(pos_sched* s, int32_t l) {
   if (s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d added twice", l);
   Layer& ly = s->layers[l];
   const bool tm = timing(s);
-  if ((rc = make_event(&ly.ev_ready, false)) || (rc = make_event(&ly.ev_gathered, tm)) ||
-      (rc = make_event(&ly.ev_done, tm)))
+  if ((rc = make_event(&ly.ev_ready, false)) || (rc = make_event(&ly.ev_gathered, false)) ||
+      (rc = make_event(&ly.ev_done, false)))
     return rc;
-  if (tm && ((rc = make_event(&ly.t_start, true)) || (rc = make_event(&ly.t_packed, true)) ||
-             (rc = make_event(&ly.t_apply0, true)) || (rc = make_event(&ly.t_apply1, true))))
-    return rc;
+  if (tm)
+    for (auto& t : ly.ring)
+      if ((rc = make_event(&t.start, true)) || (rc = make_event(&t.packed, true)) ||
+          (rc = make_event(&t.gathered, true)) || (rc = make_event(&t.a0, true)) ||
+          (rc = make_event(&t.a1, true)) || (rc = make_event(&t.done, true)))
+        return rc;
   return POS_OK;
 }
 
@@ -248,6 +294,7 @@ int pos_sched_begin(pos_sched* s, float alpha) {
   s->n_triggered = 0;
   s->alpha = alpha;
   s->in_iter = true;
+  s->iter += 1;
   return POS_OK;
 }
 
@@ -314,21 +361,27 @@ int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, fl
   if (rc) return rc;
   if (!timing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TIMING");
   Layer& ly = s->layers[l];
-  POS_CUDA_TRY(cudaEventSynchronize(ly.ev_done));
-  float a = 0, b2 = 0, c2 = 0, d = 0;
-  POS_CUDA_TRY(cudaEventElapsedTime(&a, ly.t_start, ly.t_packed));
-  if (ly.scheme == POS_SCHEME_SFB) {
-    POS_CUDA_TRY(cudaEventElapsedTime(&b2, ly.t_packed, ly.ev_gathered));
-    POS_CUDA_TRY(cudaEventElapsedTime(&c2, ly.t_apply0, ly.t_apply1));
-  } else {
-    POS_CUDA_TRY(cudaEventElapsedTime(&b2, ly.t_packed, ly.t_apply0));   // reduce-scatter
-    POS_CUDA_TRY(cudaEventElapsedTime(&c2, ly.t_apply0, ly.t_apply1));   // shard apply
-    POS_CUDA_TRY(cudaEventElapsedTime(&d, ly.t_apply1, ly.ev_done));     // all-gather
-    b2 += d;
+  for (auto& t : ly.ring)
+    if ((rc = harvest(ly, t))) return rc;
+  if (ly.n_acc == 0) POS_FAIL(POS_ESTATE, "no timed iteration of layer %d yet", l);
+  if (pack_ms) *pack_ms = (float)(ly.acc_pack / ly.n_acc);
+  if (comm_ms) *comm_ms = (float)(ly.acc_comm / ly.n_acc);
+  if (apply_ms) *apply_ms = (float)(ly.acc_apply / ly.n_acc);
+  return (int)(ly.n_acc > INT32_MAX ? INT32_MAX : ly.n_acc);
+}
+
+int pos_sched_timing_reset(pos_sched* s) {
+  clear_error();
+  POS_CHECK_ARG(s, "NULL scheduler");
+  if (!timing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TIMING");
+  for (auto& ly : s->layers) {
+    for (auto& t : ly.ring) {
+      int rc = harvest(ly, t);
+      if (rc) return rc;
+    }
+    ly.acc_pack = ly.acc_comm = ly.acc_apply = 0;
+    ly.n_acc = 0;
   }
-  if (pack_ms) *pack_ms = a;
-  if (comm_ms) *comm_ms = b2;
-  if (apply_ms) *apply_ms = c2;
   return POS_OK;
 }
 
@@ -337,10 +390,14 @@ int pos_sched_destroy(pos_sched* s) {
   if (!s) return POS_OK;
   for (auto& ly : s->layers) {
     if (ly.ev_done) cudaEventSynchronize(ly.ev_done);
-    cudaEvent_t evs[] = {ly.ev_ready, ly.ev_gathered, ly.ev_done, ly.t_start,
-                         ly.t_packed, ly.t_apply0, ly.t_apply1};
+    cudaEvent_t evs[] = {ly.ev_ready, ly.ev_gathered, ly.ev_done};
     for (cudaEvent_t e : evs)
       if (e) cudaEventDestroy(e);
+    for (auto& t : ly.ring) {
+      cudaEvent_t te[] = {t.start, t.packed, t.gathered, t.a0, t.a1, t.done};
+      for (cudaEvent_t e : te)
+        if (e) cudaEventDestroy(e);
+    }
     if (ly.gbuf) cudaFree(ly.gbuf);
   }
   for (auto st : s->pool)

@@ -144,16 +144,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100). For MN-major operands the
-// leading byte offset (LBO) is the distance between 128-byte chunks along M/N and the stride
-// byte offset (SBO) the distance between 8-row groups along K.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, version 1 (sm_100). For MN-major operands the leading byte
+// offset (LBO) is the distance between 128-byte chunks along M/N and the stride byte offset (SBO)
+// the distance between swizzle-atom row groups along K.
+//   16-bit operands: SWIZZLE_128B (layout 2) — 16-byte granules, 8-row atoms (SBO = 1024 B);
+//   32-bit (tf32) MN-major operands: SWIZZLE_128B_BASE32B (layout 1) — 32-byte granules, 4-row
+//   atoms (SBO = 512 B); the only MN-major smem layout the tensor core accepts for tf32.
+template <bool kTF32>
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo) {
+  constexpr uint32_t sbo = kTF32 ? 4 * 128 : 8 * 128;
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;  // layout: SWIZZLE_128B
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  d |= (uint64_t)(kTF32 ? 1 : 2) << 61;     // layout type
   return d;
 }
 
@@ -263,8 +268,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const uint32_t sA = sbase + stage * STAGE_BYTES, sB = sA + A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk) {
-            const uint64_t ad = smem_desc(sA + kk * UK * SWZ, BOX_BYTES, 8 * SWZ);
-            const uint64_t bd = smem_desc(sB + kk * UK * SWZ, BOX_BYTES, 8 * SWZ);
+            const uint64_t ad = smem_desc<kTF32>(sA + kk * UK * SWZ, BOX_BYTES);
+            const uint64_t bd = smem_desc<kTF32>(sB + kk * UK * SWZ, BOX_BYTES);
             umma<kTF32>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
           }
           umma_commit(b_empty + 8 * stage);   // frees the smem stage when these MMAs finish
@@ -381,7 +386,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
-               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -389,7 +395,7 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -402,11 +408,14 @@ cudaError_t launch_impl(int64_t M, int64_t N, int64_t KP, const void* G, int32_t
   const int64_t R = row_elems(M, N), Mp = m_pad(M);
   const CUtensorMapDataType dt =
       kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  // operand smem layout must match the UMMA descriptor (smem_desc<kTF32>)
+  const CUtensorMapSwizzle oswz =
+      kTF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   CUtensorMap tmA, tmB, tmW;
   const uint8_t* g = static_cast<const uint8_t*>(G);
-  if (!encode_2d(&tmA, dt, g, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK) ||
+  if (!encode_2d(&tmA, dt, g, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK, oswz) ||
       !encode_2d(&tmB, dt, g + Mp * EB, (uint64_t)N, (uint64_t)KP, (uint64_t)(R * EB), CHUNK,
-                 BK) ||
+                 BK, oswz) ||
       !encode_2d(&tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, W, (uint64_t)N, (uint64_t)M,
                  (uint64_t)(ldw * 4), WSUB, BM))
     return cudaErrorInvalidValue;
