@@ -1,0 +1,637 @@
+#!/usr/bin/env python
+"""bench.py — Poseidon per-layer gradient synchronisation on B200: per-iteration sync time,
+parameters synchronised per second, and roofline fractions (BASELINE.json metric).
+
+A "step" is one full-model synchronisation through the WFBP scheduler: every
+layer of the model is triggered in backward order L..1 and synchronised with the scheme Algorithm 1
+picks for it (SFB for FC layers, PS for CONV/BN layers), exactly as during training. Inputs
+(factors u, v for FC layers; dense gradients for the rest; fp32 weights) are synthetic, resident in
+HBM, with the shapes of the named torchvision architecture and per-GPU batch K (data-parallel weak
+scaling: K is fixed per GPU, so the work per rank grows with N only through the K*N gathered
+samples).
+
+Default workload: config c3 = VGG19-22K (229,052,817 params), K = 32 per GPU — the north_star
+target (BASELINE.json configs[3]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+Rank 0 prints ONE JSON line. `--impl reference` times the fp64 CPU oracle (oracle/, the only
+reference this tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth_inputs as si  # noqa: E402
+
+METRIC = "grad_sync_params_per_s"
+UNIT = "params/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+NVLINK_GBS_PER_DIR = 770.0   # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(PEAKS_FALLBACK, source="fallback (B200_PROFILING.md)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "tf32", "f32"])
+    ap.add_argument("--sequential", action="store_true", help="WFBP off: sync after the whole step")
+    ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--bucket-mb", type=float, default=2.0,
+                    help="PS unit = consecutive dense layers up to this many MiB of fp32 (the paper's "
+                         "2 MB KV pairs); 0 = one unit per layer")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="issue every step from the host (default: replay the step as a CUDA graph)")
+    ap.add_argument("--layers", action="store_true", help="also print a per-layer table to stderr")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    return a
+
+
+# ------------------------------------------------------------------------------ accounting --
+def plan_units(model, bucket_elems):
+    """Synchronisation units: every FC layer alone (SFB); consecutive dense layers grouped into
+    buckets of >= bucket_elems parameters (the paper's fixed-size KV pairs), a layer
+    larger than that alone. bucket_elems = 0: one unit per layer (the paper's one syncer per layer)."""
+    units, cur = [], None
+    for l, ly in enumerate(model.layers):
+        if ly.kind == "fc":
+            if cur:
+                units.append(cur)
+                cur = None
+            units.append({"kind": "fc", "layers": [l], "n": ly.params})
+            continue
+        if cur is None:
+            cur = {"kind": "dense", "layers": [], "sizes": [], "n": 0}
+        cur["layers"].append(l)
+        cur["sizes"].append(ly.n)
+        cur["n"] += ly.n
+        if cur["n"] >= bucket_elems:
+            units.append(cur)
+            cur = None
+    if cur:
+        units.append(cur)
+    return units
+
+
+def unit_accounting(model, units, K, P, dtype):
+    """Algorithmic bytes / flops per unit; never the dense all-reduce avoided."""
+    sf = 2 if dtype == "bf16" else 4
+    rows = []
+    for u in units:
+        if u["kind"] == "fc":
+            ly = model.layers[u["layers"][0]]
+            M, N = ly.M, ly.N
+            KP = K * P
+            rows.append({
+                "name": ly.name, "scheme": "SFB", "params": ly.params,
+                "hbm_a4": 8 * M * N + sf * KP * (M + N),
+                "flop_a4": 2 * M * N * KP,
+                "hbm_other": K * (M + N) * (2 + sf) + 8 * M + sf * KP * M,   # pack + bias
+                "nvl": (P - 1) * K * (M + N) * sf,
+            })
+        else:
+            S = _shard_len(u["n"], P)
+            names = [model.layers[l].name for l in u["layers"]]
+            rows.append({"name": names[0] + (f"..(+{len(names) - 1})" if len(names) > 1 else ""),
+                         "scheme": "PS", "params": u["n"],
+                         "hbm_a4": 0, "flop_a4": 0, "hbm_other": 12 * S,
+                         "nvl": 2 * (P - 1) * S * 4 if P > 1 else 0})
+    return rows
+
+
+def _shard_len(n, P):
+    """Rank 0's shard length from the library's shard table (the largest shard)."""
+    import paper_1706_03292_b200 as pos
+    lo, hi = pos.pos_shard_range(n, P, 0)
+    return hi - lo
+
+
+def roofline_times(rows, peaks, P):
+    hbm = peaks["hbm_gbs"] * 1e9
+    tc = peaks["bf16_tflops"] * 1e12
+    nvl = NVLINK_GBS_PER_DIR * 1e9
+    t_nvl = sum(r["nvl"] for r in rows) / nvl if P > 1 else 0.0
+    t_k = sum(max(r["flop_a4"] / tc, (r["hbm_a4"] + r["hbm_other"]) / hbm) for r in rows)
+    t_seq = sum((r["nvl"] / nvl if P > 1 else 0.0) + max(r["flop_a4"] / tc, (r["hbm_a4"] + r["hbm_other"]) / hbm)
+                for r in rows)
+    return max(t_nvl, t_k), t_seq, t_nvl, t_k
+
+
+# ------------------------------------------------------------------------------ clocks ------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.marks = {}
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, name):
+        self.marks[name] = time.time()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        sel = [s for (t, s) in self.samples if t0 <= t <= t1 and len(s) >= 9]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(s[1]) for s in sel if num(s[1]) is not None]
+        mx = [num(s[2]) for s in sel if num(s[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in sel for i in range(4) if s[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sel),
+                "power_w_max": max((num(s[3]) or 0.0) for s in sel)}
+
+
+# ------------------------------------------------------------------------------ our arm -----
+def _log(msg):
+    if os.environ.get("POS_BENCH_VERBOSE"):
+        print(f"[bench r{os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
+def run_ours(a):
+    import faulthandler
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    if os.environ.get("POS_BENCH_VERBOSE"):
+        faulthandler.dump_traceback_later(float(os.environ.get("POS_BENCH_WATCHDOG", "90")), exit=True)
+
+    import paper_1706_03292_b200 as pos
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == a.gpus, f"--gpus {a.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        _log("process group up")
+        ctx = pos.Context.from_torch_distributed()
+        _log("poseidon context up")
+    else:
+        ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    if a.max_ctas:
+        ctx.set_max_ctas(a.max_ctas)
+    P = world
+    model_name, K = si.CONFIGS[a.config]
+    model = si.load_model(model_name)
+    L = len(model.layers)
+    alpha = -0.01 / P
+    in_dt = pos.POS_IN_BF16 if a.dtype == "bf16" else pos.POS_IN_F32
+    fdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 * 1 + rank)
+    units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
+    sch = pos.Scheduler(ctx, L, timing=("apply" if not a.layers else True), sequential=a.sequential)
+    bufs = [None] * L
+    for un in units:
+        if un["kind"] == "fc":
+            l = un["layers"][0]
+            ly = model.layers[l]
+            M, N = ly.M, ly.N
+            W = (torch.rand(M, N, device=dev, generator=gen) * 2 - 1) / math.sqrt(N)
+            b = torch.zeros(M, device=dev) if ly.bias else None
+            u = (torch.randn(K, M, device=dev, generator=gen) * 2 ** -5).to(fdt)
+            v = torch.relu(torch.randn(K, N, device=dev, generator=gen)).to(fdt)
+            s = sch.add_fc(l, M, N, K, W, b, None, dtype=a.dtype, in_dtype=in_dt)
+            assert s == pos.POS_SCHEME_SFB, (ly, s)   # Alg. 1 at these configs
+            bufs[l] = {"kind": "fc", "W": W, "b": b, "u": u, "v": v}
+        else:
+            n = un["n"]
+            Pn = pos.pos_padded_size(n, P)
+            W = torch.zeros(Pn, device=dev)
+            W[:n] = (torch.rand(n, device=dev, generator=gen) * 2 - 1) * 0.05
+            g = torch.zeros(Pn, device=dev)
+            g[:n] = torch.randn(n, device=dev, generator=gen) * 2 ** -5
+            g0 = g.clone()
+            sch.add_dense_bucket(un["layers"][0], un["sizes"], W, g)
+            off = 0
+            for l, nl in zip(un["layers"], un["sizes"]):
+                bufs[l] = {"kind": "dense", "W": W[off:off + nl], "g": g[off:off + nl], "g0": g0[off:off + nl], "n": nl}
+                off += nl
+    main = torch.cuda.current_stream()
+
+    def step(stream):
+        sch.begin(alpha)
+        for l in range(L - 1, -1, -1):      # backward order: b^L .. b^1
+            bb = bufs[l]
+            if bb["kind"] == "fc":
+                sch.factors_ready(l, bb["u"], bb["v"], stream)
+            else:
+                sch.grad_ready(l, stream)
+        sch.end(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def refresh_grads():
+        for bb in bufs:
+            if bb["kind"] == "dense":
+                bb["g"].copy_(bb["g0"])
+
+    def capture_ring(fn, n=4):
+        """CUDA graphs of one step each: replaying them round-robin keeps n timing-event slots of
+        the scheduler live (slot = iteration mod 4), so per-kernel timings stay measurable."""
+        gs = []
+        cs = torch.cuda.Stream()
+        cs.wait_stream(main)
+        for _ in range(n):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+                fn(torch.cuda.current_stream())
+            gs.append(g)
+        main.wait_stream(cs)
+        return gs
+
+    # ---- warmup (untimed, eager: NCCL connections, launch plans) ----
+    _log(f"{len(units)} units registered; warmup")
+    for _ in range(a.warmup):
+        step(main)
+    torch.cuda.synchronize()
+    _log("warmup done")
+    graphs = g_e2e = run_e2e = None
+    if a.eager:
+        run = lambda i: step(main)
+    else:
+        graphs = capture_ring(step)
+        _log("captured")
+        run = lambda i: graphs[i % len(graphs)].replay()
+        for i in range(len(graphs)):
+            run(i)
+    torch.cuda.synchronize()
+    _log("graph warmup done")
+    refresh_grads()      # reduce-scatter sums in place; start the timed region from fresh gradients
+    torch.cuda.synchronize()
+    sch.timing_reset()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
+    e0.record(main)
+    h0 = time.perf_counter()
+    for i in range(a.steps):
+        run(i)
+    host_ms = (time.perf_counter() - h0) * 1e3 / a.steps   # host enqueue cost per step
+    e1.record(main)
+    torch.cuda.synchronize()
+    barrier()
+    t_wall1 = time.time()
+    ms = e0.elapsed_time(e1) / a.steps
+    _log(f"timed region done: {ms:.4f} ms/step")
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    unit_times = [sch.timing(un["layers"][0]) for un in units]
+    # clock soak: if the timed region was too short for the 50 ms sampler, keep the same load
+    # running (untimed) for ~1 s so the clock record describes this workload under load
+    soak_t0 = soak_t1 = None
+    if (t_wall1 - t_wall0) < 1.0:
+        soak_t0 = time.time()
+        n_soak = max(1, int(1.0 / max(ms / 1e3, 1e-5)))
+        for i in range(n_soak):
+            run(i)
+        torch.cuda.synchronize()
+        soak_t1 = time.time()
+    # the eager (no graph) step, for reference: host-launch bound for many-layer models
+    eager_ms = None
+    if not a.eager:
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(main)
+        for _ in range(a.steps):
+            step(main)
+        g1.record(main)
+        torch.cuda.synchronize()
+        eager_ms = g0.elapsed_time(g1) / a.steps
+        if world > 1:
+            t = torch.tensor([eager_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            eager_ms = float(t.item())
+
+    # ---- e2e: the same step through the public API, inputs from pinned host memory ----
+    e2e = None
+    if not a.no_e2e:
+        host_in, h2d, d2h = [], 0, 0
+        for bb in bufs:
+            if bb["kind"] == "fc":
+                hu, hv = bb["u"].cpu().pin_memory(), bb["v"].cpu().pin_memory()
+                host_in.append((hu, hv))
+                h2d += hu.numel() * hu.element_size() + hv.numel() * hv.element_size()
+            else:
+                hg = bb["g0"][:bb["n"]].cpu().pin_memory()
+                host_in.append((hg,))
+                h2d += hg.numel() * 4
+        res_dev = [bb["b"] for bb in bufs if bb["kind"] == "fc" and bb["b"] is not None]
+        res_host = [r.cpu().pin_memory() for r in res_dev]
+        d2h = sum(r.numel() * 4 for r in res_host)
+
+        def e2e_step(stream):
+            sch.begin(alpha)
+            for l in range(L - 1, -1, -1):
+                bb = bufs[l]
+                if bb["kind"] == "fc":
+                    bb["u"].copy_(host_in[l][0], non_blocking=True)
+                    bb["v"].copy_(host_in[l][1], non_blocking=True)
+                    sch.factors_ready(l, bb["u"], bb["v"], stream)
+                else:
+                    bb["g"][:bb["n"]].copy_(host_in[l][0], non_blocking=True)
+                    sch.grad_ready(l, stream)
+            sch.end(stream)
+            for r, h in zip(res_dev, res_host):
+                h.copy_(r, non_blocking=True)
+
+        if a.eager:
+            run_e2e = lambda i: e2e_step(main)
+        else:
+            g_e2e = capture_ring(e2e_step)
+            run_e2e = lambda i: g_e2e[i % len(g_e2e)].replay()
+        for i in range(4):
+            run_e2e(i)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(main)
+        for i in range(a.steps):
+            run_e2e(i)
+        f1.record(main)
+        torch.cuda.synchronize()
+        ms_e2e = f0.elapsed_time(f1) / a.steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": P * model.total_params / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "note": "per step: H2D of every layer's factors/gradients from pinned host memory, each layer "
+                       "triggered after its upload (backward order), D2H of the FC biases"
+                       + ("" if a.eager else "; step captured as a CUDA graph")}
+    clocks.stop()
+    if soak_t0 is not None:
+        clk = clocks.summary(soak_t0, soak_t1)
+        clk["window"] = "untimed soak of the same step right after the timed region (timed region < 1 s)"
+    else:
+        clk = clocks.summary(t_wall0, t_wall1)
+        clk["window"] = "timed region"
+
+    # ---- accounting & roofline ----
+    peaks = load_peaks()
+    rows = unit_accounting(model, units, K, P, a.dtype)
+    t_pipe, t_seq, t_nvl, t_kern = roofline_times(rows, peaks, P)
+    a4_bytes = sum(r["hbm_a4"] for r in rows)
+    a4_flop = sum(r["flop_a4"] for r in rows)
+    a4_ms = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "SFB")
+    ps_bytes = sum(r["hbm_other"] for r in rows if r["scheme"] == "PS")
+    ps_ms = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "PS")
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        key = f"{a.config}_P{P}_{a.dtype}"
+        if key in tj:
+            traffic = tj[key].get("a4_dram_bytes_per_step")
+    achieved = a4_bytes / (a4_ms / 1e3) / 1e9 if a4_ms > 0 else None
+    roof = {"kernel": "sfb_tc_kernel (A4 reconstruct-and-apply, all SFB layers of one step)",
+            "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"] if achieved else None,
+            "traffic": traffic,
+            "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
+            "peak_source": peaks["source"],
+            "tensor_tflops": a4_flop / (a4_ms / 1e3) / 1e12 if a4_ms > 0 else None,
+            "tensor_frac_of_bf16_peak": (a4_flop / (a4_ms / 1e3) / 1e12) / peaks["bf16_tflops"] if a4_ms > 0 else None,
+            "ps_apply": {"achieved_gbs": ps_bytes / (ps_ms / 1e3) / 1e9 if ps_ms > 0 else None,
+                         "frac": (ps_bytes / (ps_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if ps_ms > 0 else None,
+                         "algorithmic_bytes_per_step": ps_bytes, "kernel_ms_per_step": ps_ms},
+            "step": {"t_roofline_pipelined_ms": t_pipe * 1e3, "t_roofline_sequential_ms": t_seq * 1e3,
+                     "t_nvlink_ms": t_nvl * 1e3, "t_kernels_ms": t_kern * 1e3,
+                     "frac_pipelined": (t_pipe * 1e3) / ms, "nvlink_gbs_per_dir": NVLINK_GBS_PER_DIR}}
+    n_launch = 0
+    for r, un in zip(rows, units):
+        if r["scheme"] == "SFB":
+            n_launch += 3                   # pack, reconstruct-and-apply, bias
+        else:
+            lo, hi = pos.pos_shard_range(un["n"], P, rank)
+            ln = hi - lo
+            n_launch += (1 if ln >= 4 else 0) + (1 if ln % 4 else 0)
+    out = {
+        "metric": METRIC, "value": P * model.total_params / (ms / 1e3), "unit": UNIT,
+        "n_gpus": P, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": a.dtype, "data": "synthetic (random factors/gradients/weights of the named architecture's shapes)",
+        "config": {"workload": f"{model_name} full-model gradient sync ({a.config}), K={K}/GPU, "
+                               f"{'sequential (WFBP off)' if a.sequential else 'WFBP'}",
+                   "model_params": model.total_params, "layers": L,
+                   "fc_layers_sfb": sum(1 for r in rows if r["scheme"] == "SFB"),
+                   "dense_layers_ps": sum(1 for ly in model.layers if ly.kind != "fc"),
+                   "ps_units": sum(1 for r in rows if r["scheme"] == "PS"),
+                   "ps_bucket_mb": a.bucket_mb,
+                   "per_gpu_batch": K, "global_batch": K * P, "parallelism": f"dp{P}",
+                   "l2": "inputs larger than L2 (fp32 weights alone are "
+                         f"{4 * model.total_params / 2**20:.0f} MiB vs 126 MB L2)",
+                   "nccl": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}},
+        "model_params_per_s": model.total_params / (ms / 1e3),
+        "host_enqueue_ms_per_step": host_ms,
+        "launch_mode": "eager" if a.eager else "cuda_graph (4-graph ring, one step each)",
+        "eager_ms_per_step": eager_ms,
+        "roofline": roof,
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": n_launch * a.steps,
+        "gpu_launches_note": "libposeidon kernels per timed region (NCCL kernels and cudaMemsetAsync not counted)",
+    }
+    if a.layers and rank == 0:
+        for l, (r, lt) in enumerate(zip(rows, unit_times)):
+            print(f"{l:3d} {r['name']:>20s} {r['scheme']:>3s} params={r['params']:>11d} pack={lt[0]*1e3:8.1f}us "
+                  f"comm={lt[1]*1e3:8.1f}us apply={lt[2]*1e3:8.1f}us", file=sys.stderr)
+    cpu = None
+    if rank == 0 and P == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline_sample(a.config, P, a.dtype, min_seconds=10.0)
+    out["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(out), file=_JSON_OUT, flush=True)
+    # captured graphs hold NCCL resources of the communicator: free them before finalising it
+    graphs = g_e2e = run = run_e2e = None
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    sch.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- oracle (CPU) baseline ----
+def _oracle_sample(config, P, dtype):
+    """A bounded sample of the workload for the fp64 oracle: the model's 4096x4096 FC layer (or its
+    largest FC <= 2^24 params) via SFB plus its first 8 dense layers via PS, P workers."""
+    import numpy as np
+    model_name, K = si.CONFIGS[config]
+    model = si.load_model(model_name)
+    fcs = [l for l in model.layers if l.kind == "fc" and l.M * l.N <= (1 << 24)]
+    fc = max(fcs, key=lambda l: l.M * l.N)
+    dense = [l for l in model.layers if l.kind == "dense"][:8]
+    dt = "bf16" if dtype == "bf16" else "f32"
+    Us, Vs = zip(*(si.stat_factors(si.rng(7, 0, p), K, fc.M, fc.N, dt) for p in range(P)))
+    W = si.stat_weights(si.rng(7, 1), fc.M, fc.N)
+    b = np.zeros(fc.M, np.float32)
+    dense_in = [(si.stat_weights(si.rng(7, 2 + i), 1, l.n)[0],
+                 [si.stat_dense_grad(si.rng(8, i, p), l.n) for p in range(P)]) for i, l in enumerate(dense)]
+    params = fc.params + sum(l.n for l in dense)
+    desc = (f"{model_name}: {fc.name} ({fc.M}x{fc.N}, SFB, K*P={K * P}) + first {len(dense)} dense layers (PS); "
+            f"{params} params of {model.total_params}; P={P} workers")
+    return (fc, Us, Vs, W, b, dense_in), params, desc
+
+
+def _oracle_step(sample, alpha):
+    from oracle import sync   # bench.py's cpu_baseline / reference arm may execute the oracle
+    fc, Us, Vs, W, b, dense_in = sample
+    sync.sfb_update(W, b, Us, Vs, alpha)
+    for Wd, gs in dense_in:
+        sync.ps_update(Wd, gs, alpha)
+
+
+def _cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if th:
+            return int(max(th))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_baseline_sample(config, P, dtype, min_seconds=10.0):
+    sample, params, desc = _oracle_sample(config, P, dtype)
+    _oracle_step(sample, -0.01 / P)      # warm
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        _oracle_step(sample, -0.01 / P)
+        n += 1
+        if time.perf_counter() - t0 >= min_seconds:
+            break
+    dt = (time.perf_counter() - t0) / n
+    return {"value": P * params / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+            "sample": desc + f"; {n} repetitions, {dt * 1e3:.1f} ms each", "os_cpu_count": os.cpu_count()}
+
+
+def run_reference(a):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    P = a.gpus
+    sample, params, desc = _oracle_sample(a.config, P, a.dtype)
+    for _ in range(a.warmup):
+        _oracle_step(sample, -0.01 / P)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        _oracle_step(sample, -0.01 / P)
+    dt = (time.perf_counter() - t0) / a.steps
+    value = P * params / dt
+    model_name, K = si.CONFIGS[a.config]
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (same generators as the GPU arm)",
+           "config": {"workload": f"{model_name} full-model gradient sync ({a.config}), K={K}/GPU — oracle on a "
+                                  "bounded sample (see cpu_baseline.sample)", "per_gpu_batch": K,
+                      "global_batch": K * P, "parallelism": f"dp{P} (computed on host, rank 0)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": desc},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), file=_JSON_OUT, flush=True)
+
+
+_JSON_OUT = sys.stdout
+
+
+def main():
+    # The driver reads ONE JSON line from stdout: route everything else that writes to fd 1 (NCCL's
+    # version banner, library prints) to stderr, and print the result line on the saved stdout.
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -57,8 +57,10 @@ enum {
   POS_OK = 0, POS_EINVAL = -1, POS_ESTATE = -2, POS_ECUDA = -3, POS_ENCCL = -4,
   POS_ENOMEM = -5, POS_EUNSUPPORTED = -6
 };
-/* pos_sched_create flags */
-enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2 };
+/* pos_sched_create flags: TIMING = per-unit pack / collective / apply stage events;
+ * TIMING_APPLY = only the apply stage (reconstruct-and-apply, shard apply) is bracketed, which
+ * adds the fewest graph nodes; SEQUENTIAL = WFBP off (sync after the whole backward). */
+enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2, POS_SCHED_TIMING_APPLY = 4 };
 
 /* ABI version (major * 100 + minor). */
 int pos_version(void);
@@ -104,11 +106,16 @@ int64_t pos_factor_row_elems(int64_t M, int64_t N);
 
 /* Fill out_128B (128 bytes) with an ncclUniqueId. Call on rank 0, broadcast, then pos_init. */
 int pos_get_unique_id(void* out_128B);
-/* Collective over `world` processes (one per GPU); blocks until all ranks have joined. */
+/* Collective over `world` processes (one per GPU); blocks until all ranks have joined.
+ * With world > 1 the NCCL communicator is capped at POS_NCCL_MAX_CTAS CTAs (env, default 16) and
+ * the persistent reconstruction kernel leaves that many SMs (+4) free (POS_SFB_MAX_CTAS env, or
+ * pos_set_max_ctas) so collectives are never starved behind it. */
 int pos_init(const void* nccl_unique_id_128B, int32_t world, int32_t rank, pos_ctx** out);
 /* Single-GPU context simulating P_sim workers (no NCCL): for the pos_sim_* entry points and for
  * P_sim = 1 real single-GPU use. */
 int pos_init_local(int32_t P_sim, pos_ctx** out);
+/* Destroy the context. CUDA graphs that captured calls on this context must be destroyed first
+ * (they hold NCCL resources of its communicator). */
 int pos_finalize(pos_ctx* ctx);
 int pos_world(const pos_ctx* ctx);
 int pos_rank(const pos_ctx* ctx);
@@ -206,6 +213,15 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
                      int32_t dtype, float* W, float* b, float* grad, int32_t force_scheme);
 /* DENSE layer of n parameters: W and grad with pos_padded_size(n, P) elements. Returns PS. */
 int pos_sched_add_dense(pos_sched* s, int32_t l, int64_t n, float* W, float* grad);
+/* A BUCKET of `count` consecutive DENSE layers l_first .. l_first+count-1 stored back to back in
+ * one flat buffer (layer l_first+i at offset n[0]+..+n[i-1], no per-layer padding): the paper's
+ * fixed-size KV pairs as the PS unit. The bucket (sum n elements; W and grad with
+ * pos_padded_size(sum n, P) elements) is synchronised once all its layers have been triggered.
+ * Returns PS. */
+int pos_sched_add_dense_bucket(pos_sched* s, int32_t l_first, int32_t count, const int64_t* n,
+                               float* W, float* grad);
+/* Index of the synchronisation unit (layer or bucket) that layer l belongs to. */
+int pos_sched_unit_of(pos_sched* s, int32_t l);
 int pos_sched_begin(pos_sched* s, float alpha);
 int pos_sched_factors_ready(pos_sched* s, int32_t l, const void* u, const void* v, void* stream);
 int pos_sched_grad_ready(pos_sched* s, int32_t l, void* stream);
@@ -215,7 +231,7 @@ int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer);
 int pos_sched_end(pos_sched* s, void* consumer);
 /* Query: the scheme chosen for layer l. */
 int pos_sched_scheme(pos_sched* s, int32_t l);
-/* With POS_SCHED_TIMING: AVERAGE device milliseconds, over every iteration since the last reset,
+/* With POS_SCHED_TIMING(_APPLY): AVERAGE device milliseconds, over every iteration since the last reset,
  * of layer l's pack, collective(s) (all-gather; or reduce-scatter + all-gather) and apply
  * (reconstruct-and-apply; or shard apply) stages, each bracketed by CUDA events on the stream that
  * runs it. Synchronises on the layer's outstanding iterations. Returns the iteration count (> 0). */

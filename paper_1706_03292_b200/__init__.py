@@ -19,7 +19,7 @@ POS_ROLE_SERVER, POS_ROLE_WORKER, POS_ROLE_BOTH = 0, 1, 2
 POS_DT_BF16, POS_DT_TF32, POS_DT_F32 = 0, 1, 2
 POS_IN_BF16, POS_IN_F32 = 0, 1
 POS_OK, POS_EINVAL, POS_ESTATE, POS_ECUDA, POS_ENCCL, POS_ENOMEM, POS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL = 1, 2
+POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY = 1, 2, 4
 
 DTYPES = {"bf16": POS_DT_BF16, "tf32": POS_DT_TF32, "f32": POS_DT_F32}
 SCHEME_NAMES = {POS_SCHEME_PS: "PS", POS_SCHEME_SFB: "SFB", POS_SCHEME_ADAM: "ADAM"}
@@ -220,9 +220,11 @@ class Scheduler:
     """pos_sched: WFBP per-layer scheduler (Algorithm 2 on CUDA streams/events)."""
 
     def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False):
+        """timing: False | True (all stages) | "apply" (apply stage only)."""
         self.ctx = ctx
         h = C.c_void_p()
-        flags = (POS_SCHED_TIMING if timing else 0) | (POS_SCHED_SEQUENTIAL if sequential else 0)
+        tflag = POS_SCHED_TIMING_APPLY if timing == "apply" else (POS_SCHED_TIMING if timing else 0)
+        flags = tflag | (POS_SCHED_SEQUENTIAL if sequential else 0)
         _chk(lib().pos_sched_create(ctx.h, n_layers, flags, C.byref(h)), "pos_sched_create")
         self.h = h
         self.L = n_layers
@@ -233,6 +235,15 @@ class Scheduler:
 
     def add_dense(self, l, n, W, grad):
         return _chk(lib().pos_sched_add_dense(self.h, l, n, _ptr(W), _ptr(grad)), "pos_sched_add_dense")
+
+    def add_dense_bucket(self, l_first, sizes, W, grad):
+        """Consecutive dense layers l_first.. stored back to back in W / grad (flat fp32)."""
+        arr = (C.c_int64 * len(sizes))(*sizes)
+        return _chk(lib().pos_sched_add_dense_bucket(self.h, l_first, len(sizes), arr, _ptr(W), _ptr(grad)),
+                    "pos_sched_add_dense_bucket")
+
+    def unit_of(self, l):
+        return _chk(lib().pos_sched_unit_of(self.h, l), "pos_sched_unit_of")
 
     def begin(self, alpha):
         _chk(lib().pos_sched_begin(self.h, alpha), "pos_sched_begin")

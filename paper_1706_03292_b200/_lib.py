@@ -44,6 +44,8 @@ SIGNATURES = {
     "pos_sched_create": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
     "pos_sched_add_fc": (C.c_int, [vp, i32, i64, i64, i64, i32, i32, vp, vp, vp, i32]),
     "pos_sched_add_dense": (C.c_int, [vp, i32, i64, vp, vp]),
+    "pos_sched_add_dense_bucket": (C.c_int, [vp, i32, i32, P_i64, vp, vp]),
+    "pos_sched_unit_of": (C.c_int, [vp, i32]),
     "pos_sched_begin": (C.c_int, [vp, f32]),
     "pos_sched_factors_ready": (C.c_int, [vp, i32, vp, vp, vp]),
     "pos_sched_grad_ready": (C.c_int, [vp, i32, vp]),

@@ -2,6 +2,7 @@
 // by anything outside csrc/).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -48,6 +49,17 @@ inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4;
 
 int num_sms();
 
+// Record a TIMING event: a plain record outside stream capture; an external event node inside a
+// capture, so that it remains a real record when the CUDA graph is replayed.
+inline cudaError_t record_timing_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaError_t q = cudaStreamIsCapturing(s, &st);
+  if (q != cudaSuccess) return q;
+  return st == cudaStreamCaptureStatusActive
+             ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+             : cudaEventRecord(e, s);
+}
+
 // ---- kernel launchers (return cudaError_t of the launch) ----
 cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                                 const void* u, const void* v, void* slot, cudaStream_t s);
@@ -67,6 +79,19 @@ cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const
                           int32_t accumulate, float* W, int64_t ldw, float alpha, int max_ctas,
                           cudaStream_t s);
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G);
+
+// A launch plan for the tensor-core reconstruct-and-apply: TMA descriptors encoded once for fixed
+// buffers (the scheduler keeps one per SFB layer, so the hot path does no host-side encoding).
+struct SfbTcPlan {
+  CUtensorMap tmA, tmB, tmW;
+  int64_t M = 0, N = 0, KP = 0;
+  int nb_n = 0, num_tiles = 0, nkb = 0, grid = 0;
+  bool tf32 = false;
+};
+// false if the shape/alignment/dtype cannot use the tensor-core kernel
+bool sfb_tc_make_plan(SfbTcPlan* plan, int64_t M, int64_t N, int64_t KP, int32_t dtype,
+                      const void* G, float* W, int64_t ldw, int max_ctas);
+cudaError_t sfb_tc_launch(const SfbTcPlan& plan, float alpha, int accumulate, cudaStream_t s);
 
 // A4 + A4b dispatcher used by the C ABI and the context code
 int reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,

@@ -1,6 +1,7 @@
 // Context lifetime, NCCL communicator, and the one-shot per-layer synchronisation entry points
 // (SURVEY §8(a) A2-A8, §8(b)). Each entry point only validates, enqueues kernels and NCCL calls
 // on the caller's stream, and returns; no host synchronisation on the hot path.
+#include <cstdlib>
 #include <cstring>
 
 #include "ctx.h"
@@ -51,13 +52,14 @@ int ctx_workspace(pos_ctx* c, size_t bytes, void** out) {
 
 // A5 + A6 + A7 + A8 for a dense (or flattened FC) layer of n parameters, on stream s.
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done) {
+                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail) {
   const int P = c->world;
   const int64_t S = pos_shard_stride(n, P);
   if (S < 0) return (int)S;
   const int64_t padded = S * P;
   // A5: the padding tail is owned (zeroed) by the library so the reduce-scatter sums zeros there
-  if (padded > n) {
+  // (with a single worker nothing reads it)
+  if (zero_tail && P > 1 && !c->local && padded > n) {
     cudaError_t e = cudaMemsetAsync(grad + n, 0, (size_t)(padded - n) * sizeof(float), s);
     if (e != cudaSuccess) return ctx_cuda_fail(c, e, "cudaMemsetAsync(grad tail)");
   }
@@ -68,7 +70,7 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
                                         ncclSum, c->comm, s);
     if (nr != ncclSuccess) return ctx_nccl_fail(c, nr, "ncclReduceScatter");
   }
-  if (ev_rs_done) cudaEventRecord(ev_rs_done, s);
+  if (ev_rs_done) record_timing_event(ev_rs_done, s);
   // A7: apply on the owned shard
   int64_t lo = 0, hi = n;
   if (!c->local) {
@@ -78,7 +80,7 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
     cudaError_t e = launch_ps_apply(grad + lo, W + lo, hi - lo, alpha, s);
     if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_apply launch");
   }
-  if (ev_apply_done) cudaEventRecord(ev_apply_done, s);
+  if (ev_apply_done) record_timing_event(ev_apply_done, s);
   if (P > 1 && !c->local) {
     // A8: in-place all-gather of the fresh shards
     ncclResult_t nr = ncclAllGather(W + (int64_t)r * S, W, (size_t)S, ncclFloat32, c->comm, s);
@@ -128,6 +130,11 @@ int pos_get_unique_id(void* out_128B) {
   return POS_OK;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 static int ctx_common_init(pos_ctx* c) {
   POS_CUDA_TRY(cudaGetDevice(&c->device));
   int lo = 0, hi = 0;
@@ -149,12 +156,19 @@ int pos_init(const void* uid, int32_t world, int32_t rank, pos_ctx** out) {
   if (world > 1) {
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    // NCCL's CTAs must find free SMs while the persistent reconstruction kernel runs: cap them
+    // (maxCTAs) and keep the same number of SMs out of the reconstruction grid (max_ctas).
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    const int nccl_ctas = env_int("POS_NCCL_MAX_CTAS", 16);
+    cfg.maxCTAs = nccl_ctas;
+    cfg.commName = "poseidon";
+    ncclResult_t r = ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg);
     if (r != ncclSuccess) {
       cudaStreamDestroy(c->comm_stream);
       delete c;
-      return ctx_nccl_fail(nullptr, r, "ncclCommInitRank");
+      return ctx_nccl_fail(nullptr, r, "ncclCommInitRankConfig");
     }
+    c->max_ctas = env_int("POS_SFB_MAX_CTAS", num_sms() - nccl_ctas - 4);
   }
   *out = c;
   return POS_OK;
@@ -178,6 +192,7 @@ int pos_finalize(pos_ctx* c) {
   clear_error();
   if (!c) return POS_OK;
   int rc = POS_OK;
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->comm) {
     ncclResult_t r = ncclCommDestroy(c->comm);
     if (r != ncclSuccess) rc = POS_ENCCL;
@@ -248,7 +263,7 @@ int pos_sync_layer_ps(pos_ctx* c, int64_t n, float* grad, float* W, float alpha,
                 "simulated context with P > 1: use pos_sim_sync_layer_ps");
   int rc = ctx_check(c);
   if (rc) return rc;
-  return stage_ps_dense(c, n, grad, W, alpha, (cudaStream_t)stream, nullptr, nullptr);
+  return stage_ps_dense(c, n, grad, W, alpha, (cudaStream_t)stream, nullptr, nullptr, true);
 }
 
 int pos_sync_layer_fc_ps(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
@@ -266,7 +281,8 @@ int pos_sync_layer_fc_ps(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in
   if ((rc = ctx_workspace(c, (size_t)(K * row_elems(M, N) * dtype_bytes(dtype)), &buf))) return rc;
   if ((rc = stage_fc_local_grad(c, M, N, K, in_dtype, dtype, u, v, buf, grad, has_bias, s)))
     return rc;
-  return stage_ps_dense(c, M * N + (has_bias ? M : 0), grad, Wb, alpha, s, nullptr, nullptr);
+  return stage_ps_dense(c, M * N + (has_bias ? M : 0), grad, Wb, alpha, s, nullptr, nullptr,
+                        true);
 }
 
 // ---------------------------------------------------------------------- simulated workers --

@@ -33,8 +33,10 @@ inline ncclDataType_t nccl_type(int32_t dtype) {
 }
 
 // stages shared by the one-shot entry points and the scheduler
+// zero_tail: zero grad[n, P*S) first (the one-shot API; the scheduler zeroes it once at add time
+// and the tail stays zero because the in-place reduce-scatter only ever sums zeros into it).
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done);
+                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail);
 int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
                         int32_t dtype, const void* u, const void* v, void* pack_buf, float* grad,
                         int32_t has_bias, cudaStream_t s);

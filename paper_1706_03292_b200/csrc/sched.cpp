@@ -1,28 +1,34 @@
 // WFBP scheduler — wait-free backpropagation (§3.1) as Algorithm 2
 // on CUDA streams and events instead of a CPU thread pool.
 //
-//  * one record per layer = the paper's "syncer", with its scheme fixed at
-//    registration by Algorithm 1 ("choose the optimal method even before the
-//    communication happens");
+//  * one "syncer" per layer; its scheme is fixed at registration by Algorithm 1
+//    ("choose the optimal method even before the communication happens");
+//  * the synchronisation UNIT is a layer, or a BUCKET of consecutive dense layers laid out in one
+//    flat buffer — the paper's fixed-size KV pairs (PAPER:258, 2 MB) as the unit of PS traffic.
+//    A bucket is synchronised once all of its layers have been triggered;
 //  * a trigger (pos_sched_factors_ready / pos_sched_grad_ready) is Alg. 2 L7
 //    "thread_pool.Schedule(sync(l))": it records an event on the producer (backward) stream and
-//    enqueues the layer's sync behind that event, so s^l overlaps b^i for i < l;
-//  * all collectives go on ONE high-priority comm stream in trigger order (the same L..1 order on
-//    every rank — a requirement of NCCL); the heavy SFB reconstruct-and-apply runs on a pool of
-//    apply streams (the paper's GPU stream pool);
-//  * the binary vector C is one completion event per layer; pos_sched_end makes the
-//    consumer stream wait for all of them (Alg. 2 L8 "wait_until(sync_count == num_layers)").
+//    enqueues the unit's sync behind it, so s^l overlaps b^i for i < l;
+//  * with collectives (P > 1) every NCCL call goes on ONE high-priority comm stream in trigger
+//    order (the same L..1 order on every rank, as NCCL requires); the heavy SFB
+//    reconstruct-and-apply runs on an apply stream. Without collectives (P = 1) there is no comm
+//    hop: SFB units run on apply stream 0 and dense units spread over apply streams 1..3 (the
+//    paper's GPU stream pool);
+//  * the binary vector C is one completion event per unit; pos_sched_end makes the
+//    consumer stream wait for all of them (Alg. 2 L8 "wait_until(sync_count == num_layers)");
 //  * POS_SCHED_SEQUENTIAL defers every sync until pos_sched_end, behind an event recorded on the
 //    consumer stream: the "sync after the whole backward" baseline (Fig. 3a; the
-//    Caffe+PS comparison of PAPER:407).
+//    Caffe+PS comparison of PAPER:407);
+//  * iterations may be captured into CUDA graphs: nothing here synchronises with the host while
+//    a stream is capturing, and timing events become external event nodes.
 #include <vector>
 
 #include "ctx.h"
 
 namespace {
 
-constexpr int kPool = 4;
-constexpr int kTRing = 4;   // timing event sets per layer (iterations in flight)
+constexpr int kPool = 4;    // apply streams
+constexpr int kTRing = 4;   // timing event sets per unit (iterations in flight)
 
 struct TSlot {
   cudaEvent_t start = nullptr, packed = nullptr, gathered = nullptr, a0 = nullptr, a1 = nullptr,
@@ -30,8 +36,8 @@ struct TSlot {
   bool used = false;
 };
 
-struct Layer {
-  bool added = false;
+// A synchronisation unit: one FC layer, one dense layer, or a bucket of dense layers.
+struct Unit {
   int kind = POS_KIND_DENSE;
   int scheme = POS_SCHEME_PS;
   int64_t M = 0, N = 0, K = 0, n = 0;
@@ -39,15 +45,27 @@ struct Layer {
   float* W = nullptr;
   float* b = nullptr;
   float* grad = nullptr;
-  void* gbuf = nullptr;   // SFB: P*K rows of the gathered factors; FC-on-PS: K rows (local)
-  cudaEvent_t ev_ready = nullptr, ev_gathered = nullptr, ev_done = nullptr;
+  void* gbuf = nullptr;        // SFB: P*K gathered factor rows; FC-on-PS: K local rows
+  pos::SfbTcPlan plan;         // cached TMA descriptors of the tensor-core reconstruction
+  bool has_plan = false;
+  int plan_ctas = -1;
+  std::vector<int> members;    // layer indices (forward order)
+  int pending = 0;             // members not yet triggered in this iteration
+  const void* u = nullptr;     // FC factors of this iteration
+  const void* v = nullptr;
+  cudaEvent_t ev_gathered = nullptr, ev_done = nullptr;
   TSlot ring[kTRing];
   double acc_pack = 0, acc_comm = 0, acc_apply = 0;
   int64_t n_acc = 0;
+  int seq = 0;                 // registration order (stream assignment)
+};
+
+struct Layer {
+  bool added = false;
+  int kind = POS_KIND_DENSE;
+  int unit = -1;
   bool triggered = false;
-  const void* u = nullptr;
-  const void* v = nullptr;
-  int64_t trig_seq = -1;
+  cudaEvent_t ev_ready = nullptr;
 };
 
 }  // namespace
@@ -57,107 +75,141 @@ struct pos_sched {
   int L = 0;
   int flags = 0;
   std::vector<Layer> layers;
+  std::vector<Unit> units;
   cudaStream_t pool[kPool] = {};
   bool in_iter = false;
   float alpha = 0.0f;
   int n_triggered = 0;
-  std::vector<int> order;  // trigger order of the current iteration
+  std::vector<int> order;  // unit issue order of the current iteration
   cudaEvent_t ev_end = nullptr;
   int64_t iter = 0;        // iterations begun
+  bool captured = false;   // some iteration was issued under CUDA-graph stream capture
 };
 
 using namespace pos;
 
 namespace {
 
-bool timing(const pos_sched* s) { return (s->flags & POS_SCHED_TIMING) != 0; }
+bool timing_full(const pos_sched* s) { return (s->flags & POS_SCHED_TIMING) != 0; }
+bool timing_any(const pos_sched* s) {
+  return (s->flags & (POS_SCHED_TIMING | POS_SCHED_TIMING_APPLY)) != 0;
+}
 
 int make_event(cudaEvent_t* e, bool timed) {
   POS_CUDA_TRY(cudaEventCreateWithFlags(e, timed ? cudaEventDefault : cudaEventDisableTiming));
   return POS_OK;
 }
 
-// Fold a finished iteration's timing events into the layer's running sums.
-int harvest(Layer& ly, TSlot& t) {
-  if (!t.used) return POS_OK;
-  POS_CUDA_TRY(cudaEventSynchronize(t.done));
-  float pack = 0, comm = 0, apply = 0, extra = 0;
-  POS_CUDA_TRY(cudaEventElapsedTime(&pack, t.start, t.packed));
-  if (ly.scheme == POS_SCHEME_SFB) {
-    POS_CUDA_TRY(cudaEventElapsedTime(&comm, t.packed, t.gathered));   // all-gather
-    POS_CUDA_TRY(cudaEventElapsedTime(&apply, t.a0, t.a1));            // reconstruct-and-apply
-  } else {
-    POS_CUDA_TRY(cudaEventElapsedTime(&comm, t.packed, t.a0));         // reduce-scatter
-    POS_CUDA_TRY(cudaEventElapsedTime(&apply, t.a0, t.a1));            // shard apply
-    POS_CUDA_TRY(cudaEventElapsedTime(&extra, t.a1, t.done));          // all-gather
-    comm += extra;
-  }
-  ly.acc_pack += pack;
-  ly.acc_comm += comm;
-  ly.acc_apply += apply;
-  ly.n_acc += 1;
-  t.used = false;
+int trec(cudaEvent_t e, cudaStream_t st) {
+  if (!e) return POS_OK;
+  POS_CUDA_TRY(record_timing_event(e, st));
   return POS_OK;
 }
 
-// Enqueue sync(l) behind ly.ev_ready.
-int issue_layer(pos_sched* s, int l) {
+bool is_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive;
+}
+
+// Fold a finished iteration's timing events into the unit's running sums. Under graph replay the
+// slot's events are re-recorded by every replay of the graph that owns them, so the slot stays
+// `used` (keep_used) and each harvest samples the latest replay.
+int harvest(Unit& u, TSlot& t, bool keep_used = false) {
+  if (!t.used) return POS_OK;
+  POS_CUDA_TRY(cudaEventSynchronize(t.a1));
+  float pack = 0, comm = 0, apply = 0, extra = 0;
+  POS_CUDA_TRY(cudaEventElapsedTime(&apply, t.a0, t.a1));
+  if (t.start) {
+    POS_CUDA_TRY(cudaEventSynchronize(t.done));
+    POS_CUDA_TRY(cudaEventElapsedTime(&pack, t.start, t.packed));
+    if (u.scheme == POS_SCHEME_SFB) {
+      POS_CUDA_TRY(cudaEventElapsedTime(&comm, t.packed, t.gathered));   // all-gather
+    } else {
+      POS_CUDA_TRY(cudaEventElapsedTime(&comm, t.packed, t.a0));         // reduce-scatter
+      POS_CUDA_TRY(cudaEventElapsedTime(&extra, t.a1, t.done));          // all-gather
+      comm += extra;
+    }
+  }
+  u.acc_pack += pack;
+  u.acc_comm += comm;
+  u.acc_apply += apply;
+  u.n_acc += 1;
+  t.used = keep_used;
+  return POS_OK;
+}
+
+// Enqueue sync(unit) behind the ready events of all its member layers.
+int issue_unit(pos_sched* s, int ui, bool capturing) {
   pos_ctx* c = s->ctx;
-  Layer& ly = s->layers[l];
-  cudaStream_t cs = c->comm_stream;
-  const bool tm = timing(s);
+  Unit& un = s->units[ui];
   const int P = c->world;
+  const bool coll = P > 1;                 // collectives needed?
   TSlot* ts = nullptr;
-  if (tm) {
-    ts = &ly.ring[(s->iter - 1) % kTRing];
-    int rc0 = harvest(ly, *ts);
-    if (rc0) return rc0;
+  int rc = POS_OK;
+  if (timing_any(s)) {
+    ts = &un.ring[(s->iter - 1) % kTRing];
+    if (!capturing && (rc = harvest(un, *ts))) return rc;   // no host sync inside a capture
     ts->used = true;
   }
-  POS_CUDA_TRY(cudaStreamWaitEvent(cs, ly.ev_ready, 0));
+  // stream of the first stage: the comm stream when a collective follows, else an apply stream
+  cudaStream_t as = un.scheme == POS_SCHEME_SFB ? s->pool[0] : s->pool[1 + un.seq % (kPool - 1)];
+  cudaStream_t cs = coll ? c->comm_stream : as;
+  for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_ready, 0));
   if (s->flags & POS_SCHED_SEQUENTIAL) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_end, 0));
-  if (tm) POS_CUDA_TRY(cudaEventRecord(ts->start, cs));
-  int rc = POS_OK;
-  if (ly.scheme == POS_SCHEME_SFB) {
-    const int64_t R = row_elems(ly.M, ly.N), slot = ly.K * R;
+  if (ts && (rc = trec(ts->start, cs))) return rc;
+  if (un.scheme == POS_SCHEME_SFB) {
+    const int64_t R = row_elems(un.M, un.N), slot = un.K * R;
     uint8_t* my_slot =
-        static_cast<uint8_t*>(ly.gbuf) + (size_t)(c->rank * slot * dtype_bytes(ly.dtype));
+        static_cast<uint8_t*>(un.gbuf) + (size_t)(c->rank * slot * dtype_bytes(un.dtype));
     // Move(GPU2CPU) analogue: A2 pack into this rank's slot
-    cudaError_t e = launch_pack_factors(ly.M, ly.N, ly.K, ly.in_dtype, ly.dtype, ly.u, ly.v,
+    cudaError_t e = launch_pack_factors(un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v,
                                         my_slot, cs);
     if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack launch");
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->packed, cs));
-    // Send + Receive: A3 all-gather of the factors
-    if (P > 1) {
-      ncclResult_t r = ncclAllGather(my_slot, ly.gbuf, (size_t)slot, nccl_type(ly.dtype), c->comm, cs);
+    if (ts && (rc = trec(ts->packed, cs))) return rc;
+    if (coll) {
+      // Send + Receive: A3 all-gather of the factors
+      ncclResult_t r =
+          ncclAllGather(my_slot, un.gbuf, (size_t)slot, nccl_type(un.dtype), c->comm, cs);
       if (r != ncclSuccess) return ctx_nccl_fail(c, r, "ncclAllGather(factors)");
+      if (ts && (rc = trec(ts->gathered, cs))) return rc;
+      POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));   // sync events last: joins a capture
+      POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
+    } else if (ts && (rc = trec(ts->gathered, cs))) {
+      return rc;
     }
-    POS_CUDA_TRY(cudaEventRecord(ly.ev_gathered, cs));
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->gathered, cs));
-    // Move(CPU2GPU) analogue: A4 + A4b on an apply stream
-    cudaStream_t as = s->pool[l % kPool];
-    POS_CUDA_TRY(cudaStreamWaitEvent(as, ly.ev_gathered, 0));
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->a0, as));
-    rc = reconstruct_apply(ly.M, ly.N, ly.K * P, ly.dtype, ly.gbuf, 1, ly.W, ly.N, ly.b, s->alpha,
-                           c->max_ctas, as);
-    if (rc != POS_OK) { if (c->sticky == POS_OK) c->sticky = rc; return rc; }
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->a1, as));
-    POS_CUDA_TRY(cudaEventRecord(ly.ev_done, as));
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->done, as));
+    // Move(CPU2GPU) analogue: A4 + A4b on the apply stream
+    if (ts && (rc = trec(ts->a0, as))) return rc;
+    if (un.plan_ctas != c->max_ctas) {   // (re)build the cached launch plan
+      un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * P, un.dtype, un.gbuf, un.W,
+                                     un.N, c->max_ctas);
+      un.plan_ctas = c->max_ctas;
+    }
+    if (un.has_plan) {
+      cudaError_t e2 = sfb_tc_launch(un.plan, s->alpha, 1, as);
+      if (e2 == cudaSuccess && un.b)
+        e2 = launch_bias_colsum(un.M, un.N, un.K * P, un.dtype, un.gbuf, 1, un.b, s->alpha, as);
+      if (e2 != cudaSuccess) return ctx_cuda_fail(c, e2, "reconstruct launch");
+    } else {
+      rc = reconstruct_apply(un.M, un.N, un.K * P, un.dtype, un.gbuf, 1, un.W, un.N, un.b,
+                             s->alpha, c->max_ctas, as);
+      if (rc != POS_OK) { if (c->sticky == POS_OK) c->sticky = rc; return rc; }
+    }
+    if (ts && (rc = trec(ts->a1, as))) return rc;
+    if (ts && (rc = trec(ts->done, as))) return rc;
+    POS_CUDA_TRY(cudaEventRecord(un.ev_done, as));
   } else {
-    int64_t n = ly.n;
-    if (ly.kind == POS_KIND_FC) {
+    if (un.kind == POS_KIND_FC) {
       // FC layer on the PS path: local dense gradient from the factors first
-      rc = stage_fc_local_grad(c, ly.M, ly.N, ly.K, ly.in_dtype, ly.dtype, ly.u, ly.v, ly.gbuf,
-                               ly.grad, ly.b != nullptr, cs);
+      rc = stage_fc_local_grad(c, un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v, un.gbuf,
+                               un.grad, un.b != nullptr, cs);
       if (rc != POS_OK) return rc;
     }
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->packed, cs));
-    rc = stage_ps_dense(c, n, ly.grad, ly.W, s->alpha, cs, tm ? ts->a0 : nullptr,
-                        tm ? ts->a1 : nullptr);
+    if (ts && (rc = trec(ts->packed, cs))) return rc;
+    rc = stage_ps_dense(c, un.n, un.grad, un.W, s->alpha, cs, ts ? ts->a0 : nullptr,
+                        ts ? ts->a1 : nullptr, /*zero_tail=*/false);
     if (rc != POS_OK) return rc;
-    POS_CUDA_TRY(cudaEventRecord(ly.ev_done, cs));
-    if (tm) POS_CUDA_TRY(cudaEventRecord(ts->done, cs));
+    if (ts && (rc = trec(ts->done, cs))) return rc;
+    POS_CUDA_TRY(cudaEventRecord(un.ev_done, cs));
   }
   return POS_OK;
 }
@@ -174,10 +226,49 @@ int trigger(pos_sched* s, int32_t l, cudaStream_t st) {
   if (ly.triggered) POS_FAIL(POS_ESTATE, "layer %d triggered twice in one iteration", l);
   POS_CUDA_TRY(cudaEventRecord(ly.ev_ready, st));
   ly.triggered = true;
-  ly.trig_seq = s->n_triggered++;
-  s->order.push_back(l);
+  s->n_triggered++;
+  Unit& un = s->units[ly.unit];
+  if (--un.pending > 0) return POS_OK;      // bucket: wait for its remaining layers
+  s->order.push_back(ly.unit);
   if (s->flags & POS_SCHED_SEQUENTIAL) return POS_OK;  // deferred to pos_sched_end
-  return issue_layer(s, l);
+  const bool cap = is_capturing(st);
+  s->captured |= cap;
+  return issue_unit(s, ly.unit, cap);
+}
+
+int new_unit(pos_sched* s, Unit&& u, int* out) {
+  const bool tf = timing_full(s), ta = timing_any(s);
+  int rc;
+  if ((rc = make_event(&u.ev_gathered, false)) || (rc = make_event(&u.ev_done, false))) return rc;
+  if (ta)
+    for (auto& t : u.ring) {
+      if ((rc = make_event(&t.a0, true)) || (rc = make_event(&t.a1, true))) return rc;
+      if (tf && ((rc = make_event(&t.start, true)) || (rc = make_event(&t.packed, true)) ||
+                 (rc = make_event(&t.gathered, true)) || (rc = make_event(&t.done, true))))
+        return rc;
+    }
+  u.seq = (int)s->units.size();
+  s->units.push_back(std::move(u));
+  *out = (int)s->units.size() - 1;
+  return POS_OK;
+}
+
+int add_layer(pos_sched* s, int32_t l, int kind, int unit) {
+  Layer& ly = s->layers[l];
+  int rc = make_event(&ly.ev_ready, false);
+  if (rc) return rc;
+  ly.kind = kind;
+  ly.unit = unit;
+  ly.added = true;
+  return POS_OK;
+}
+
+int check_add(pos_sched* s, int32_t l) {
+  int rc = check_layer(s, l);
+  if (rc) return rc;
+  if (s->in_iter) POS_FAIL(POS_ESTATE, "add after begin");
+  if (s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d added twice", l);
+  return POS_OK;
 }
 
 }  // namespace
@@ -188,13 +279,16 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   clear_error();
   POS_CHECK_ARG(c && out, "NULL argument");
   POS_CHECK_ARG(n_layers >= 1, "n_layers must be >= 1");
-  POS_CHECK_ARG((flags & ~(POS_SCHED_TIMING | POS_SCHED_SEQUENTIAL)) == 0, "unknown flags");
+  POS_CHECK_ARG(
+      (flags & ~(POS_SCHED_TIMING | POS_SCHED_SEQUENTIAL | POS_SCHED_TIMING_APPLY)) == 0,
+      "unknown flags");
   POS_CHECK_ARG(!c->local || c->world == 1, "the scheduler needs a real (or 1-worker) context");
   pos_sched* s = new pos_sched();
   s->ctx = c;
   s->L = n_layers;
   s->flags = flags;
   s->layers.resize(n_layers);
+  s->units.reserve(n_layers);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   for (int i = 0; i < kPool; ++i) {
@@ -209,29 +303,10 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   return POS_OK;
 }
 
-static int add_common(pos_sched* s, int32_t l) {
-  int rc = check_layer(s, l);
-  if (rc) return rc;
-  if (s->in_iter) POS_FAIL(POS_ESTATE, "add after begin");
-  if (s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d added twice", l);
-  Layer& ly = s->layers[l];
-  const bool tm = timing(s);
-  if ((rc = make_event(&ly.ev_ready, false)) || (rc = make_event(&ly.ev_gathered, false)) ||
-      (rc = make_event(&ly.ev_done, false)))
-    return rc;
-  if (tm)
-    for (auto& t : ly.ring)
-      if ((rc = make_event(&t.start, true)) || (rc = make_event(&t.packed, true)) ||
-          (rc = make_event(&t.gathered, true)) || (rc = make_event(&t.a0, true)) ||
-          (rc = make_event(&t.a1, true)) || (rc = make_event(&t.done, true)))
-        return rc;
-  return POS_OK;
-}
-
 int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
                      int32_t dtype, float* W, float* b, float* grad, int32_t force_scheme) {
   clear_error();
-  int rc = check_layer(s, l);
+  int rc = check_add(s, l);
   if (rc) return rc;
   pos_ctx* c = s->ctx;
   POS_CHECK_ARG(M >= 1 && N >= 1 && K >= 1 && M <= (1LL << 31) && N <= (1LL << 31),
@@ -250,35 +325,56 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
     POS_CHECK_ARG(!b || b == W + M * N, "FC layer on the PS path needs b == W + M*N");
     POS_CHECK_ARG(aligned16(W) && aligned16(grad), "W and grad must be 16-byte aligned");
   }
-  if ((rc = add_common(s, l))) return rc;
-  Layer& ly = s->layers[l];
-  ly.kind = POS_KIND_FC;
-  ly.scheme = scheme;
-  ly.M = M; ly.N = N; ly.K = K; ly.n = n;
-  ly.in_dtype = in_dtype; ly.dtype = dtype;
-  ly.W = W; ly.b = b; ly.grad = grad;
+  Unit u;
+  u.kind = POS_KIND_FC;
+  u.scheme = scheme;
+  u.M = M; u.N = N; u.K = K; u.n = n;
+  u.in_dtype = in_dtype; u.dtype = dtype;
+  u.W = W; u.b = b; u.grad = grad;
+  u.members = {l};
   const int64_t rows = scheme == POS_SCHEME_SFB ? K * c->world : K;
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));
-  cudaError_t e = cudaMalloc(&ly.gbuf, bytes);
+  cudaError_t e = cudaMalloc(&u.gbuf, bytes);
   if (e != cudaSuccess) { (void)cudaGetLastError(); POS_FAIL(POS_ENOMEM, "cudaMalloc(%zu)", bytes); }
-  ly.added = true;
+  if (scheme == POS_SCHEME_PS) {
+    const int64_t padded = pos_padded_size(n, c->world);
+    if (padded > n) POS_CUDA_TRY(cudaMemset(grad + n, 0, (size_t)(padded - n) * sizeof(float)));
+  }
+  int ui;
+  if ((rc = new_unit(s, std::move(u), &ui)) || (rc = add_layer(s, l, POS_KIND_FC, ui))) return rc;
   return scheme;
 }
 
-int pos_sched_add_dense(pos_sched* s, int32_t l, int64_t n, float* W, float* grad) {
+int pos_sched_add_dense_bucket(pos_sched* s, int32_t l_first, int32_t count, const int64_t* n,
+                               float* W, float* grad) {
   clear_error();
-  int rc = check_layer(s, l);
-  if (rc) return rc;
-  POS_CHECK_ARG(n >= 1, "n must be >= 1");
+  POS_CHECK_ARG(s && n && count >= 1, "bad arguments");
   POS_CHECK_ARG(W && grad && aligned16(W) && aligned16(grad), "W, grad: non-NULL, 16-byte aligned");
-  if ((rc = add_common(s, l))) return rc;
-  Layer& ly = s->layers[l];
-  ly.kind = POS_KIND_DENSE;
-  ly.scheme = POS_SCHEME_PS;
-  ly.n = n;
-  ly.W = W; ly.grad = grad;
-  ly.added = true;
+  int64_t total = 0;
+  for (int i = 0; i < count; ++i) {
+    int rc = check_add(s, l_first + i);
+    if (rc) return rc;
+    POS_CHECK_ARG(n[i] >= 1, "layer %d: n must be >= 1", l_first + i);
+    total += n[i];
+  }
+  Unit u;
+  u.kind = POS_KIND_DENSE;
+  u.scheme = POS_SCHEME_PS;
+  u.n = total;
+  u.W = W; u.grad = grad;
+  for (int i = 0; i < count; ++i) u.members.push_back(l_first + i);
+  const int64_t padded = pos_padded_size(total, s->ctx->world);
+  if (padded > total)
+    POS_CUDA_TRY(cudaMemset(grad + total, 0, (size_t)(padded - total) * sizeof(float)));
+  int ui, rc;
+  if ((rc = new_unit(s, std::move(u), &ui))) return rc;
+  for (int i = 0; i < count; ++i)
+    if ((rc = add_layer(s, l_first + i, POS_KIND_DENSE, ui))) return rc;
   return POS_SCHEME_PS;
+}
+
+int pos_sched_add_dense(pos_sched* s, int32_t l, int64_t n, float* W, float* grad) {
+  return pos_sched_add_dense_bucket(s, l, 1, &n, W, grad);
 }
 
 int pos_sched_begin(pos_sched* s, float alpha) {
@@ -289,7 +385,8 @@ int pos_sched_begin(pos_sched* s, float alpha) {
     if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d was never added", l);
   int rc = ctx_check(s->ctx);
   if (rc) return rc;
-  for (auto& ly : s->layers) { ly.triggered = false; ly.trig_seq = -1; }  // C := 0
+  for (auto& ly : s->layers) ly.triggered = false;   // C := 0
+  for (auto& un : s->units) un.pending = (int)un.members.size();
   s->order.clear();
   s->n_triggered = 0;
   s->alpha = alpha;
@@ -303,10 +400,10 @@ int pos_sched_factors_ready(pos_sched* s, int32_t l, const void* u, const void* 
   int rc = check_layer(s, l);
   if (rc) return rc;
   Layer& ly = s->layers[l];
-  if (ly.kind != POS_KIND_FC) POS_FAIL(POS_ESTATE, "layer %d is not an FC layer", l);
+  if (!ly.added || ly.kind != POS_KIND_FC) POS_FAIL(POS_ESTATE, "layer %d is not an FC layer", l);
   POS_CHECK_ARG(u && v, "NULL factors");
-  ly.u = u;
-  ly.v = v;
+  s->units[ly.unit].u = u;
+  s->units[ly.unit].v = v;
   return trigger(s, l, (cudaStream_t)stream);
 }
 
@@ -314,7 +411,8 @@ int pos_sched_grad_ready(pos_sched* s, int32_t l, void* stream) {
   clear_error();
   int rc = check_layer(s, l);
   if (rc) return rc;
-  if (s->layers[l].kind != POS_KIND_DENSE) POS_FAIL(POS_ESTATE, "layer %d is not a dense layer", l);
+  Layer& ly = s->layers[l];
+  if (!ly.added || ly.kind != POS_KIND_DENSE) POS_FAIL(POS_ESTATE, "layer %d is not a dense layer", l);
   return trigger(s, l, (cudaStream_t)stream);
 }
 
@@ -322,8 +420,11 @@ int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer) {
   clear_error();
   int rc = check_layer(s, l);
   if (rc) return rc;
-  if (!s->layers[l].triggered && s->in_iter) POS_FAIL(POS_ESTATE, "layer %d not triggered yet", l);
-  POS_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)consumer, s->layers[l].ev_done, 0));
+  Layer& ly = s->layers[l];
+  if (!ly.added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
+  if (s->in_iter && s->units[ly.unit].pending > 0)
+    POS_FAIL(POS_ESTATE, "the unit of layer %d has not been issued yet", l);
+  POS_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)consumer, s->units[ly.unit].ev_done, 0));
   return POS_OK;
 }
 
@@ -337,12 +438,14 @@ int pos_sched_end(pos_sched* s, void* consumer) {
   cudaStream_t cs = (cudaStream_t)consumer;
   if (s->flags & POS_SCHED_SEQUENTIAL) {
     POS_CUDA_TRY(cudaEventRecord(s->ev_end, cs));
-    for (int l : s->order) {
-      int rc = issue_layer(s, l);
+    const bool cap = is_capturing(cs);
+    s->captured |= cap;
+    for (int u : s->order) {
+      int rc = issue_unit(s, u, cap);
       if (rc) { s->in_iter = false; return rc; }
     }
   }
-  for (auto& ly : s->layers) POS_CUDA_TRY(cudaStreamWaitEvent(cs, ly.ev_done, 0));
+  for (auto& un : s->units) POS_CUDA_TRY(cudaStreamWaitEvent(cs, un.ev_done, 0));
   s->in_iter = false;
   return ctx_check(s->ctx);
 }
@@ -352,54 +455,66 @@ int pos_sched_scheme(pos_sched* s, int32_t l) {
   int rc = check_layer(s, l);
   if (rc) return rc;
   if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
-  return s->layers[l].scheme;
+  return s->units[s->layers[l].unit].scheme;
 }
 
 int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, float* apply_ms) {
   clear_error();
   int rc = check_layer(s, l);
   if (rc) return rc;
-  if (!timing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TIMING");
-  Layer& ly = s->layers[l];
-  for (auto& t : ly.ring)
-    if ((rc = harvest(ly, t))) return rc;
-  if (ly.n_acc == 0) POS_FAIL(POS_ESTATE, "no timed iteration of layer %d yet", l);
-  if (pack_ms) *pack_ms = (float)(ly.acc_pack / ly.n_acc);
-  if (comm_ms) *comm_ms = (float)(ly.acc_comm / ly.n_acc);
-  if (apply_ms) *apply_ms = (float)(ly.acc_apply / ly.n_acc);
-  return (int)(ly.n_acc > INT32_MAX ? INT32_MAX : ly.n_acc);
+  if (!timing_any(s)) POS_FAIL(POS_ESTATE, "scheduler created without timing");
+  if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
+  Unit& un = s->units[s->layers[l].unit];
+  for (auto& t : un.ring)
+    if ((rc = harvest(un, t, s->captured))) return rc;
+  if (un.n_acc == 0) POS_FAIL(POS_ESTATE, "no timed iteration of layer %d yet", l);
+  if (pack_ms) *pack_ms = (float)(un.acc_pack / un.n_acc);
+  if (comm_ms) *comm_ms = (float)(un.acc_comm / un.n_acc);
+  if (apply_ms) *apply_ms = (float)(un.acc_apply / un.n_acc);
+  return (int)(un.n_acc > INT32_MAX ? INT32_MAX : un.n_acc);
 }
 
 int pos_sched_timing_reset(pos_sched* s) {
   clear_error();
   POS_CHECK_ARG(s, "NULL scheduler");
-  if (!timing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TIMING");
-  for (auto& ly : s->layers) {
-    for (auto& t : ly.ring) {
-      int rc = harvest(ly, t);
-      if (rc) return rc;
+  if (!timing_any(s)) POS_FAIL(POS_ESTATE, "scheduler created without timing");
+  for (auto& un : s->units) {
+    if (!s->captured) {                   // eager: retire in-flight slots; graph: keep them live
+      for (auto& t : un.ring) {
+        int rc = harvest(un, t);
+        if (rc) return rc;
+      }
     }
-    ly.acc_pack = ly.acc_comm = ly.acc_apply = 0;
-    ly.n_acc = 0;
+    un.acc_pack = un.acc_comm = un.acc_apply = 0;
+    un.n_acc = 0;
   }
   return POS_OK;
+}
+
+int pos_sched_unit_of(pos_sched* s, int32_t l) {
+  clear_error();
+  int rc = check_layer(s, l);
+  if (rc) return rc;
+  if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
+  return s->layers[l].unit;
 }
 
 int pos_sched_destroy(pos_sched* s) {
   clear_error();
   if (!s) return POS_OK;
-  for (auto& ly : s->layers) {
-    if (ly.ev_done) cudaEventSynchronize(ly.ev_done);
-    cudaEvent_t evs[] = {ly.ev_ready, ly.ev_gathered, ly.ev_done};
-    for (cudaEvent_t e : evs)
-      if (e) cudaEventDestroy(e);
-    for (auto& t : ly.ring) {
+  for (auto& un : s->units) {
+    if (un.ev_done) cudaEventSynchronize(un.ev_done);
+    if (un.ev_gathered) cudaEventDestroy(un.ev_gathered);
+    if (un.ev_done) cudaEventDestroy(un.ev_done);
+    for (auto& t : un.ring) {
       cudaEvent_t te[] = {t.start, t.packed, t.gathered, t.a0, t.a1, t.done};
       for (cudaEvent_t e : te)
         if (e) cudaEventDestroy(e);
     }
-    if (ly.gbuf) cudaFree(ly.gbuf);
+    if (un.gbuf) cudaFree(un.gbuf);
   }
+  for (auto& ly : s->layers)
+    if (ly.ev_ready) cudaEventDestroy(ly.ev_ready);
   for (auto st : s->pool)
     if (st) cudaStreamDestroy(st);
   if (s->ev_end) cudaEventDestroy(s->ev_end);

@@ -401,8 +401,8 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 }
 
 template <bool kTF32>
-cudaError_t launch_impl(int64_t M, int64_t N, int64_t KP, const void* G, int32_t accumulate,
-                        float* W, int64_t ldw, float alpha, int max_ctas, cudaStream_t s) {
+bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
+                    int64_t ldw, int max_ctas) {
   constexpr int EB = kTF32 ? 4 : 2;
   constexpr int BK = SWZ / EB, CHUNK = SWZ / EB;
   const int64_t R = row_elems(M, N), Mp = m_pad(M);
@@ -411,21 +411,30 @@ cudaError_t launch_impl(int64_t M, int64_t N, int64_t KP, const void* G, int32_t
   // operand smem layout must match the UMMA descriptor (smem_desc<kTF32>)
   const CUtensorMapSwizzle oswz =
       kTF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
-  CUtensorMap tmA, tmB, tmW;
   const uint8_t* g = static_cast<const uint8_t*>(G);
-  if (!encode_2d(&tmA, dt, g, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK, oswz) ||
-      !encode_2d(&tmB, dt, g + Mp * EB, (uint64_t)N, (uint64_t)KP, (uint64_t)(R * EB), CHUNK,
-                 BK, oswz) ||
-      !encode_2d(&tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, W, (uint64_t)N, (uint64_t)M,
+  if (!encode_2d(&pl->tmA, dt, g, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK,
+                 oswz) ||
+      !encode_2d(&pl->tmB, dt, g + Mp * EB, (uint64_t)N, (uint64_t)KP, (uint64_t)(R * EB),
+                 CHUNK, BK, oswz) ||
+      !encode_2d(&pl->tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, W, (uint64_t)N, (uint64_t)M,
                  (uint64_t)(ldw * 4), WSUB, BM))
-    return cudaErrorInvalidValue;
-  TileInfo ti;
-  ti.M = M; ti.N = N; ti.KP = KP;
-  ti.nb_n = (int)((N + BN - 1) / BN);
-  const int64_t tiles = (int64_t)ti.nb_n * ((M + BM - 1) / BM);
-  if (tiles > INT32_MAX) return cudaErrorInvalidValue;
-  ti.num_tiles = (int)tiles;
-  ti.nkb = (int)((KP + BK - 1) / BK);
+    return false;
+  pl->M = M; pl->N = N; pl->KP = KP;
+  pl->nb_n = (int)((N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)pl->nb_n * ((M + BM - 1) / BM);
+  if (tiles > INT32_MAX) return false;
+  pl->num_tiles = (int)tiles;
+  pl->nkb = (int)((KP + BK - 1) / BK);
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  if (grid > pl->num_tiles) grid = pl->num_tiles;
+  pl->grid = grid;
+  pl->tf32 = kTF32;
+  return true;
+}
+
+template <bool kTF32>
+cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32>,
@@ -433,10 +442,11 @@ cudaError_t launch_impl(int64_t M, int64_t N, int64_t KP, const void* G, int32_t
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  int grid = num_sms();
-  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  if (grid > ti.num_tiles) grid = ti.num_tiles;
-  sfb_tc_kernel<kTF32><<<grid, THREADS, SMEM_TOTAL, s>>>(tmA, tmB, tmW, ti, alpha, accumulate);
+  TileInfo ti;
+  ti.M = pl.M; ti.N = pl.N; ti.KP = pl.KP;
+  ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
+  sfb_tc_kernel<kTF32><<<pl.grid, THREADS, SMEM_TOTAL, s>>>(pl.tmA, pl.tmB, pl.tmW, ti, alpha,
+                                                              accumulate);
   return cudaGetLastError();
 }
 
@@ -446,12 +456,24 @@ bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
   return (ldw % 4) == 0 && aligned16(W) && aligned16(G) && N >= 1 && get_encode() != nullptr;
 }
 
+bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t dtype,
+                      const void* G, float* W, int64_t ldw, int max_ctas) {
+  if (dtype == POS_DT_F32 || !sfb_tc_supported(N, ldw, W, G)) return false;
+  if (dtype == POS_DT_TF32) return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas);
+  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas);
+}
+
+cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
+  return pl.tf32 ? launch_plan_impl<true>(pl, alpha, accumulate, s)
+                 : launch_plan_impl<false>(pl, alpha, accumulate, s);
+}
+
 cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                           int32_t accumulate, float* W, int64_t ldw, float alpha, int max_ctas,
                           cudaStream_t s) {
-  if (dtype == POS_DT_TF32)
-    return launch_impl<true>(M, N, KP, G, accumulate, W, ldw, alpha, max_ctas, s);
-  return launch_impl<false>(M, N, KP, G, accumulate, W, ldw, alpha, max_ctas, s);
+  SfbTcPlan pl;
+  if (!sfb_tc_make_plan(&pl, M, N, KP, dtype, G, W, ldw, max_ctas)) return cudaErrorInvalidValue;
+  return sfb_tc_launch(pl, alpha, accumulate, s);
 }
 
 }  // namespace pos

@@ -182,3 +182,113 @@ def test_input_validation():
         c1 = pos.Context.from_unique_id(bytes(128), 1, 0)
         c1.sync_layer_ps(100, g[1:], g[1:])   # misaligned
     assert e.value.code == pos.POS_EINVAL
+
+
+def test_sched_cuda_graph_replay_matches_oracle():
+    """The scheduler step captured as a CUDA graph (timing on): two replays equal two oracle syncs."""
+    model = make_model(4)
+    a = si.EXACT_ALPHA
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, len(model), timing=True)
+    dev = []
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            n = d["n"]
+            P = pos.pos_padded_size(n, 1)
+            W = torch.zeros(P, device="cuda"); W[:n] = to_dev(d["W"])
+            G = torch.zeros(P, device="cuda"); G[:n] = to_dev(d["g"])
+            sch.add_dense(l, n, W, G)
+            dev.append({"W": W, "G": G})        # keep G alive: the scheduler holds its pointer
+        elif d["force"] is None:
+            W, b = to_dev(d["W"]), to_dev(d["b"])
+            sch.add_fc(l, d["M"], d["N"], d["K"], W, b, None, dtype="bf16", in_dtype=pos.POS_IN_BF16)
+            dev.append({"W": W, "b": b, "u": to_dev(d["u"], "bf16"), "v": to_dev(d["v"], "bf16")})
+        else:
+            M, N, K = d["M"], d["N"], d["K"]
+            n = M * N + M
+            flat = torch.zeros(pos.pos_padded_size(n, 1), device="cuda")
+            flat[:M * N] = to_dev(d["W"]).reshape(-1)
+            flat[M * N:n] = to_dev(d["b"])
+            W, b = flat[:M * N].view(M, N), flat[M * N:n]
+            grad = torch.empty_like(flat)      # must outlive the scheduler (it keeps the pointer)
+            sch.add_fc(l, M, N, K, W, b, grad, dtype="bf16", in_dtype=pos.POS_IN_BF16,
+                       force_scheme=pos.POS_SCHEME_PS)
+            dev.append({"W": W, "b": b, "grad": grad, "u": to_dev(d["u"], "bf16"), "v": to_dev(d["v"], "bf16")})
+
+    def step(stream):
+        sch.begin(a)
+        for l in reversed(range(len(model))):
+            if model[l]["kind"] == "dense":
+                sch.grad_ready(l, stream)
+            else:
+                sch.factors_ready(l, dev[l]["u"], dev[l]["v"], stream)
+        sch.end(stream)
+
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+        step(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    # capture enqueues nothing: weights unchanged so far
+    assert np.array_equal(to_host(dev[0]["W"][:model[0]["n"]]), model[0]["W"].astype(np.float64))
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            r1 = sync.ps_update(d["W"], [d["g"]], a)
+            ref = sync.ps_update(r1, [d["g"]], a)
+            assert np.array_equal(to_host(dev[l]["W"][:d["n"]]), ref)
+        else:
+            W1, b1 = sync.sfb_update(d["W"], d["b"], [d["u"]], [d["v"]], a)
+            W2, b2 = sync.sfb_update(W1, b1, [d["u"]], [d["v"]], a)
+            assert np.array_equal(to_host(dev[l]["W"]), W2)
+            assert np.array_equal(to_host(dev[l]["b"]), b2)
+    pk, cm, ap = sch.timing(2)          # timing events are real records under replay
+    assert ap > 0
+    sch.close()
+    ctx.close()
+
+
+@pytest.mark.parametrize("timing", [False, "apply", True])
+def test_sched_dense_bucket(timing):
+    """Consecutive dense layers synchronised as one bucket (the paper's KV-pair unit): each
+    layer's parameters equal the oracle; the bucket is issued only after all its layers trigger."""
+    sizes = [1792, 36928, 73856, 5]
+    n = sum(sizes)
+    a = si.EXACT_ALPHA
+    Ws = [si.exact_weights(si.rng(30, i), k) for i, k in enumerate(sizes)]
+    Gs = [si.exact_dense_grad(si.rng(31, i), k) for i, k in enumerate(sizes)]
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, len(sizes) + 1, timing=timing)
+    Pn = pos.pos_padded_size(n, 1)
+    W = torch.zeros(Pn, device="cuda"); W[:n] = to_dev(np.concatenate(Ws))
+    G = torch.zeros(Pn, device="cuda"); G[:n] = to_dev(np.concatenate(Gs))
+    assert sch.add_dense_bucket(0, sizes, W, G) == pos.POS_SCHEME_PS
+    assert len({sch.unit_of(l) for l in range(len(sizes))}) == 1
+    Wl = torch.zeros(pos.pos_padded_size(77, 1), device="cuda")
+    wl = si.exact_weights(si.rng(32), 77); gl = si.exact_dense_grad(si.rng(33), 77)
+    Wl[:77] = to_dev(wl)
+    Gl = torch.zeros_like(Wl); Gl[:77] = to_dev(gl)
+    sch.add_dense(len(sizes), 77, Wl, Gl)
+    sch.begin(a)
+    sch.grad_ready(4)
+    for l in (3, 2, 1):
+        sch.grad_ready(l)
+    with pytest.raises(pos.PoseidonError):
+        sch.wait_layer(2)                 # bucket not issued yet (layer 0 pending)
+    sch.grad_ready(0)
+    sch.end()
+    torch.cuda.synchronize()
+    got = to_host(W[:n])
+    off = 0
+    for w, g in zip(Ws, Gs):
+        assert np.array_equal(got[off:off + len(w)], sync.ps_update(w, [g], a))
+        off += len(w)
+    assert np.array_equal(to_host(Wl[:77]), sync.ps_update(wl, [gl], a))
+    if timing:
+        assert sch.timing(0)[2] > 0
+    sch.close()
+    ctx.close()
