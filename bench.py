@@ -69,6 +69,8 @@ def parse():
                          "2 MB KV pairs); 0 = one unit per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-symm", action="store_true",
+                    help="P > 1: keep PS buffers and SFB gather buffers out of symmetric (NVLS) memory, i.e. use the stock NCCL collectives")
     ap.add_argument("--eager", action="store_true",
                     help="issue every step from the host (default: replay the step as a CUDA graph)")
     ap.add_argument("--layers", action="store_true", help="also print a per-layer table to stderr")
@@ -247,7 +249,8 @@ def run_ours(a):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * 1 + rank)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
-    sch = pos.Scheduler(ctx, L, timing=("apply" if not a.layers else True), sequential=a.sequential)
+    sch = pos.Scheduler(ctx, L, timing=("apply" if not a.layers else True), sequential=a.sequential,
+                        symm=not a.no_symm)
     bufs = [None] * L
     for un in units:
         if un["kind"] == "fc":
@@ -264,9 +267,10 @@ def run_ours(a):
         else:
             n = un["n"]
             Pn = pos.pos_padded_size(n, P)
-            W = torch.zeros(Pn, device=dev)
+            symm = P > 1 and not a.no_symm       # NVLS fused PS kernel needs symmetric W and grad
+            W = ctx.sym_empty(Pn) if symm else torch.zeros(Pn, device=dev)
             W[:n] = (torch.rand(n, device=dev, generator=gen) * 2 - 1) * 0.05
-            g = torch.zeros(Pn, device=dev)
+            g = ctx.sym_empty(Pn) if symm else torch.zeros(Pn, device=dev)
             g[:n] = torch.randn(n, device=dev, generator=gen) * 2 ** -5
             g0 = g.clone()
             sch.add_dense_bucket(un["layers"][0], un["sizes"], W, g)
@@ -498,6 +502,7 @@ def run_ours(a):
                    "dense_layers_ps": sum(1 for ly in model.layers if ly.kind != "fc"),
                    "ps_units": sum(1 for r in rows if r["scheme"] == "PS"),
                    "ps_bucket_mb": a.bucket_mb,
+                   "collectives": ("nccl" if (P == 1 or a.no_symm) else "fused NVLS kernels (symmetric memory)") if P > 1 else "none (P = 1)",
                    "per_gpu_batch": K, "global_batch": K * P, "parallelism": f"dp{P}",
                    "l2": "inputs larger than L2 (fp32 weights alone are "
                          f"{4 * model.total_params / 2**20:.0f} MiB vs 126 MB L2)",

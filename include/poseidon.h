@@ -60,7 +60,8 @@ enum {
 /* pos_sched_create flags: TIMING = per-unit pack / collective / apply stage events;
  * TIMING_APPLY = only the apply stage (reconstruct-and-apply, shard apply) is bracketed, which
  * adds the fewest graph nodes; SEQUENTIAL = WFBP off (sync after the whole backward). */
-enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2, POS_SCHED_TIMING_APPLY = 4 };
+enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2, POS_SCHED_TIMING_APPLY = 4,
+       POS_SCHED_NO_SYMM = 8 /* keep SFB gather buffers out of symmetric memory (NCCL path) */ };
 
 /* ABI version (major * 100 + minor). */
 int pos_version(void);
@@ -121,6 +122,17 @@ int pos_world(const pos_ctx* ctx);
 int pos_rank(const pos_ctx* ctx);
 /* Sticky asynchronous CUDA/NCCL error (POS_OK if none). */
 int pos_get_async_error(pos_ctx* ctx);
+/* Symmetric (NVLink-SHARP multicast) memory, NEXT-1 of SURVEY §8(f). COLLECTIVE: every rank calls
+ * with the same size in the same order. The buffer is an NCCL symmetric window on an NVLS
+ * multicast object, zero-filled. When a PS layer's W and grad both live in such buffers, its
+ * synchronisation (reduce-scatter + shard apply + all-gather) runs as ONE fused kernel:
+ * multimem.ld_reduce of the gradient shard through the switch, apply, multimem.st of the fresh W
+ * to every replica, between two cross-GPU barriers. The scheduler also places SFB gather buffers
+ * there (unless POS_SCHED_NO_SYMM) and multicasts the packed factors into them. Needs world > 1. */
+int pos_mem_alloc(pos_ctx* ctx, int64_t bytes, void** out);
+int pos_mem_free(pos_ctx* ctx, void* ptr);
+/* 1 if [ptr, ptr+bytes) lies inside one pos_mem_alloc buffer, else 0. */
+int pos_mem_is_symmetric(pos_ctx* ctx, const void* ptr, int64_t bytes);
 /* Cap the number of CTAs of the persistent SFB reconstruction kernel (0 = one per SM). Lets the
  * sync leave SMs to the concurrent backward pass (SURVEY §7 hard part 3). */
 int pos_set_max_ctas(pos_ctx* ctx, int32_t max_ctas);

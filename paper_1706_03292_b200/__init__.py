@@ -19,7 +19,7 @@ POS_ROLE_SERVER, POS_ROLE_WORKER, POS_ROLE_BOTH = 0, 1, 2
 POS_DT_BF16, POS_DT_TF32, POS_DT_F32 = 0, 1, 2
 POS_IN_BF16, POS_IN_F32 = 0, 1
 POS_OK, POS_EINVAL, POS_ESTATE, POS_ECUDA, POS_ENCCL, POS_ENOMEM, POS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY = 1, 2, 4
+POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY, POS_SCHED_NO_SYMM = 1, 2, 4, 8
 
 DTYPES = {"bf16": POS_DT_BF16, "tf32": POS_DT_TF32, "f32": POS_DT_F32}
 SCHEME_NAMES = {POS_SCHEME_PS: "PS", POS_SCHEME_SFB: "SFB", POS_SCHEME_ADAM: "ADAM"}
@@ -179,6 +179,26 @@ class Context:
     def set_max_ctas(self, n: int):
         _chk(lib().pos_set_max_ctas(self.h, n), "pos_set_max_ctas")
 
+    def sym_empty(self, numel: int, dtype=None):
+        """A zero-filled fp32 torch tensor in symmetric (NVLS multicast) memory — pos_mem_alloc.
+        COLLECTIVE: all ranks call it with the same size in the same order. Freed with the context."""
+        import torch
+        dtype = torch.float32 if dtype is None else dtype
+        nbytes = numel * torch.empty(0, dtype=dtype).element_size()
+        p = C.c_void_p()
+        _chk(lib().pos_mem_alloc(self.h, nbytes, C.byref(p)), "pos_mem_alloc")
+
+        class _Holder:
+            __cuda_array_interface__ = {"shape": (numel,), "typestr": {torch.float32: "<f4", torch.bfloat16: "<V2"}.get(dtype, "<f4"),
+                                        "data": (p.value, False), "version": 3}
+        t = torch.as_tensor(_Holder(), device=torch.device("cuda", torch.cuda.current_device()))
+        if dtype != torch.float32:
+            t = t.view(dtype)
+        return t
+
+    def is_symmetric(self, t) -> bool:
+        return bool(lib().pos_mem_is_symmetric(self.h, C.c_void_p(t.data_ptr()), t.numel() * t.element_size()))
+
     # one-shot syncs ---------------------------------------------------------------------
     def sync_layer_sfb(self, u, v, W, b=None, alpha=1.0, dtype="bf16", stream=None):
         """pos_sync_layer_sfb: W += alpha * sum over all ranks' samples of u v^T (and b += alpha * sum u)."""
@@ -219,12 +239,13 @@ class Context:
 class Scheduler:
     """pos_sched: WFBP per-layer scheduler (Algorithm 2 on CUDA streams/events)."""
 
-    def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False):
-        """timing: False | True (all stages) | "apply" (apply stage only)."""
+    def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False, symm=True):
+        """timing: False | True (all stages) | "apply" (apply stage only). symm: place SFB gather
+        buffers in symmetric memory (multicast factor pack) when world > 1."""
         self.ctx = ctx
         h = C.c_void_p()
         tflag = POS_SCHED_TIMING_APPLY if timing == "apply" else (POS_SCHED_TIMING if timing else 0)
-        flags = tflag | (POS_SCHED_SEQUENTIAL if sequential else 0)
+        flags = tflag | (POS_SCHED_SEQUENTIAL if sequential else 0) | (0 if symm else POS_SCHED_NO_SYMM)
         _chk(lib().pos_sched_create(ctx.h, n_layers, flags, C.byref(h)), "pos_sched_create")
         self.h = h
         self.L = n_layers

@@ -8,7 +8,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libposeidon.so")
+LIB_PATH = os.environ.get("POS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libposeidon.so")
 
 i32, i64, u64, f32, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_void_p
 P_i64, P_u64, P_f32 = C.POINTER(C.c_int64), C.POINTER(C.c_uint64), C.POINTER(C.c_float)
@@ -32,6 +32,9 @@ SIGNATURES = {
     "pos_rank": (C.c_int, [vp]),
     "pos_get_async_error": (C.c_int, [vp]),
     "pos_set_max_ctas": (C.c_int, [vp, i32]),
+    "pos_mem_alloc": (C.c_int, [vp, i64, C.POINTER(vp)]),
+    "pos_mem_free": (C.c_int, [vp, vp]),
+    "pos_mem_is_symmetric": (C.c_int, [vp, vp, i64]),
     "pos_pack_factors": (C.c_int, [i64, i64, i64, i32, i32, vp, vp, vp, vp]),
     "pos_reconstruct_apply": (C.c_int, [i64, i64, i64, i32, vp, i32, vp, i64, vp, f32, vp]),
     "pos_ps_apply": (C.c_int, [vp, vp, i64, f32, vp]),

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libposeidon.so")
-SOURCES = ["host.cpp", "ctx.cpp", "sched.cpp", "mem_kernels.cu", "sfb_simt.cu", "sfb_tc.cu"]
+SOURCES = ["host.cpp", "ctx.cpp", "sched.cpp", "mem_kernels.cu", "sfb_simt.cu", "sfb_tc.cu", "symm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -51,9 +51,12 @@ def _needs(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """Build libposeidon.so (or, with `defines` / `out`, an experiment variant in its own build dir)."""
     nccl_inc, nccl_lib = _nccl_dirs()
-    os.makedirs(BUILD, exist_ok=True)
+    lib_path = out or LIB
+    bdir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(bdir, exist_ok=True)
     headers = [os.path.join(ROOT, "include", "poseidon.h")] + [
         os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
     nvcc = _nvcc()
@@ -61,10 +64,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(bdir, src + ".o")
         objs.append(obj)
         if force or _needs(obj, [path] + headers):
-            cmd = [nvcc] + _flags(nccl_inc) + ["-x", "cu" if src.endswith(".cu") else "c++"]
+            cmd = [nvcc] + _flags(nccl_inc) + [f"-D{d}" for d in defines] + ["-x", "cu" if src.endswith(".cu") else "c++"]
             if src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"] if verbose else []
             cmd += ["-c", path, "-o", obj]
@@ -80,15 +83,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 sys.stderr.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
             if p.returncode:
                 raise RuntimeError(f"nvcc failed ({p.returncode}) for {cmd[-3]}")
-    if force or jobs or _needs(LIB, objs):
-        cmd = [nvcc] + ARCH + ["-shared", "-o", LIB] + objs + [
+    if force or jobs or _needs(lib_path, objs):
+        cmd = [nvcc] + ARCH + ["-shared", "-o", lib_path] + objs + [
             "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or p.returncode:
             sys.stderr.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
         if p.returncode:
             raise RuntimeError("link of libposeidon.so failed")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":

@@ -49,6 +49,12 @@ inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4;
 
 int num_sms();
 
+// Kernel launches report errors only through the runtime's last-error state, which other runtime
+// or NCCL calls may have left set (non-sticky, already reported to their callers). Clear it right
+// before launching so the check after the launch sees only the launch's own error; sticky device
+// faults are unaffected (every later call keeps returning them).
+inline void clear_stale_launch_error() { (void)cudaGetLastError(); }
+
 // Record a TIMING event: a plain record outside stream capture; an external event node inside a
 // capture, so that it remains a real record when the CUDA graph is replayed.
 inline cudaError_t record_timing_event(cudaEvent_t e, cudaStream_t s) {

@@ -56,6 +56,11 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
   const int P = c->world;
   const int64_t S = pos_shard_stride(n, P);
   if (S < 0) return (int)S;
+  {  // NVLS fused kernel when grad and W live in symmetric memory (NEXT-1)
+    bool done = false;
+    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done);
+    if (rc != POS_OK || done) return rc;
+  }
   const int64_t padded = S * P;
   // A5: the padding tail is owned (zeroed) by the library so the reduce-scatter sums zeros there
   // (with a single worker nothing reads it)
@@ -70,7 +75,7 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
                                         ncclSum, c->comm, s);
     if (nr != ncclSuccess) return ctx_nccl_fail(c, nr, "ncclReduceScatter");
   }
-  if (ev_rs_done) record_timing_event(ev_rs_done, s);
+  if (ev_rs_done) POS_CUDA_TRY(record_timing_event(ev_rs_done, s));
   // A7: apply on the owned shard
   int64_t lo = 0, hi = n;
   if (!c->local) {
@@ -80,7 +85,7 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
     cudaError_t e = launch_ps_apply(grad + lo, W + lo, hi - lo, alpha, s);
     if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_apply launch");
   }
-  if (ev_apply_done) record_timing_event(ev_apply_done, s);
+  if (ev_apply_done) POS_CUDA_TRY(record_timing_event(ev_apply_done, s));
   if (P > 1 && !c->local) {
     // A8: in-place all-gather of the fresh shards
     ncclResult_t nr = ncclAllGather(W + (int64_t)r * S, W, (size_t)S, ncclFloat32, c->comm, s);
@@ -193,6 +198,7 @@ int pos_finalize(pos_ctx* c) {
   if (!c) return POS_OK;
   int rc = POS_OK;
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  symm_destroy(c);
   if (c->comm) {
     ncclResult_t r = ncclCommDestroy(c->comm);
     if (r != ncclSuccess) rc = POS_ENCCL;

@@ -16,6 +16,7 @@ struct pos_ctx {
   void* ws = nullptr;    // one-shot workspace (grow-only)
   size_t ws_bytes = 0;
   int sticky = POS_OK;   // first asynchronous error seen
+  void* symm = nullptr;  // symmetric-memory state (symm.cu): NCCL device comm + windows
 };
 
 namespace pos {
@@ -40,5 +41,16 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
 int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
                         int32_t dtype, const void* u, const void* v, void* pack_buf, float* grad,
                         int32_t has_bias, cudaStream_t s);
+
+// symmetric-memory (NVLS) path, symm.cu
+void symm_destroy(pos_ctx* c);
+// fused reduce-scatter + apply + all-gather over NVLS when grad and W are symmetric; *done = false
+// (and nothing enqueued) otherwise
+int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
+                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done);
+// pack this rank's factors and multicast them into every rank's gather buffer (+ barrier) when the
+// gather buffer is symmetric; *done = false otherwise
+int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
+                 const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done);
 
 }  // namespace pos

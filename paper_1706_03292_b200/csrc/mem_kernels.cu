@@ -166,6 +166,7 @@ int grid_for(int64_t work_items, int threads) {
 
 cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                                 const void* u, const void* v, void* slot, cudaStream_t s) {
+  clear_stale_launch_error();
   const int64_t Mp = m_pad(M), R = row_elems(M, N);
   const int threads = 128;
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
@@ -200,6 +201,7 @@ cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtyp
 
 cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                                int32_t accumulate, float* b, float alpha, cudaStream_t s) {
+  clear_stale_launch_error();
   const int64_t R = row_elems(M, N);
   const unsigned blocks = (unsigned)((M + 31) / 32);
   if (dtype == POS_DT_BF16)
@@ -212,6 +214,7 @@ cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, 
 }
 
 cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s) {
+  clear_stale_launch_error();
   const int threads = 256;
   if (aligned16(g) && aligned16(W)) {
     const int64_t n4 = count / 4;
@@ -230,6 +233,7 @@ cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha
 
 cudaError_t launch_sim_ps_reduce_apply(const float* const* grads, int P, float* W, int64_t n,
                                        float alpha, cudaStream_t s) {
+  clear_stale_launch_error();
   GradPtrs gp{};
   for (int p = 0; p < P; ++p) gp.p[p] = grads[p];
   const int threads = 256;

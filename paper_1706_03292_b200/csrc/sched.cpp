@@ -46,6 +46,7 @@ struct Unit {
   float* b = nullptr;
   float* grad = nullptr;
   void* gbuf = nullptr;        // SFB: P*K gathered factor rows; FC-on-PS: K local rows
+  bool gbuf_symm = false;      // gbuf from pos_mem_alloc (NVLS multicast target)
   pos::SfbTcPlan plan;         // cached TMA descriptors of the tensor-core reconstruction
   bool has_plan = false;
   int plan_ctas = -1;
@@ -161,12 +162,23 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
     const int64_t R = row_elems(un.M, un.N), slot = un.K * R;
     uint8_t* my_slot =
         static_cast<uint8_t*>(un.gbuf) + (size_t)(c->rank * slot * dtype_bytes(un.dtype));
-    // Move(GPU2CPU) analogue: A2 pack into this rank's slot
-    cudaError_t e = launch_pack_factors(un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v,
-                                        my_slot, cs);
-    if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack launch");
+    // Move(GPU2CPU) + Send + Receive, fused over NVLS when the gather buffer is symmetric
+    bool mc = false;
+    if (coll && (rc = symm_pack_mc(c, un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v, un.gbuf,
+                                   cs, &mc)))
+      return rc;
+    if (!mc) {
+      // A2 pack into this rank's slot
+      cudaError_t e = launch_pack_factors(un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v,
+                                          my_slot, cs);
+      if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack launch");
+    }
     if (ts && (rc = trec(ts->packed, cs))) return rc;
-    if (coll) {
+    if (coll && mc) {
+      if (ts && (rc = trec(ts->gathered, cs))) return rc;
+      POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));
+      POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
+    } else if (coll) {
       // Send + Receive: A3 all-gather of the factors
       ncclResult_t r =
           ncclAllGather(my_slot, un.gbuf, (size_t)slot, nccl_type(un.dtype), c->comm, cs);
@@ -279,9 +291,9 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   clear_error();
   POS_CHECK_ARG(c && out, "NULL argument");
   POS_CHECK_ARG(n_layers >= 1, "n_layers must be >= 1");
-  POS_CHECK_ARG(
-      (flags & ~(POS_SCHED_TIMING | POS_SCHED_SEQUENTIAL | POS_SCHED_TIMING_APPLY)) == 0,
-      "unknown flags");
+  POS_CHECK_ARG((flags & ~(POS_SCHED_TIMING | POS_SCHED_SEQUENTIAL | POS_SCHED_TIMING_APPLY |
+                            POS_SCHED_NO_SYMM)) == 0,
+                "unknown flags");
   POS_CHECK_ARG(!c->local || c->world == 1, "the scheduler needs a real (or 1-worker) context");
   pos_sched* s = new pos_sched();
   s->ctx = c;
@@ -334,8 +346,16 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   u.members = {l};
   const int64_t rows = scheme == POS_SCHEME_SFB ? K * c->world : K;
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));
-  cudaError_t e = cudaMalloc(&u.gbuf, bytes);
-  if (e != cudaSuccess) { (void)cudaGetLastError(); POS_FAIL(POS_ENOMEM, "cudaMalloc(%zu)", bytes); }
+  if (scheme == POS_SCHEME_SFB && c->world > 1 && !c->local && (s->flags & POS_SCHED_NO_SYMM) == 0) {
+    // gather buffer in symmetric memory: the factors are multicast straight into it (collective,
+    // every rank registers its layers in the same order)
+    if (pos_mem_alloc(c, (int64_t)bytes, &u.gbuf) == POS_OK) u.gbuf_symm = true;
+    else clear_error();
+  }
+  if (!u.gbuf) {
+    cudaError_t e = cudaMalloc(&u.gbuf, bytes);
+    if (e != cudaSuccess) { (void)cudaGetLastError(); POS_FAIL(POS_ENOMEM, "cudaMalloc(%zu)", bytes); }
+  }
   if (scheme == POS_SCHEME_PS) {
     const int64_t padded = pos_padded_size(n, c->world);
     if (padded > n) POS_CUDA_TRY(cudaMemset(grad + n, 0, (size_t)(padded - n) * sizeof(float)));
@@ -511,7 +531,10 @@ int pos_sched_destroy(pos_sched* s) {
       for (cudaEvent_t e : te)
         if (e) cudaEventDestroy(e);
     }
-    if (un.gbuf) cudaFree(un.gbuf);
+    if (un.gbuf) {
+      if (un.gbuf_symm) pos_mem_free(s->ctx, un.gbuf);
+      else cudaFree(un.gbuf);
+    }
   }
   for (auto& ly : s->layers)
     if (ly.ev_ready) cudaEventDestroy(ly.ev_ready);

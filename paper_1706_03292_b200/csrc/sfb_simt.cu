@@ -78,6 +78,7 @@ sfb_simt_kernel(const T* __restrict__ U, const T* __restrict__ V, int64_t R, int
 cudaError_t launch_sfb_simt(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                             int32_t accumulate, float* W, int64_t ldw, float alpha,
                             cudaStream_t s) {
+  clear_stale_launch_error();
   const int64_t R = row_elems(M, N), Mp = m_pad(M);
   const int64_t gy = (M + TM - 1) / TM, gx = (N + TN - 1) / TN;
   if (gy > 65535) return cudaErrorInvalidValue;

@@ -32,13 +32,25 @@ namespace {
 
 constexpr int BM = 128;             // tile rows (m) = UMMA M = TMEM lanes
 constexpr int BN = 256;             // tile cols (n) = UMMA N = TMEM columns per accumulator
-constexpr int STAGES = 3;           // operand ring depth
-constexpr int WSLOTS = 4;           // W sub-tile ring depth
+#ifndef POS_SFB_STAGES
+#define POS_SFB_STAGES 3
+#endif
+#ifndef POS_SFB_WSLOTS
+#define POS_SFB_WSLOTS 5
+#endif
+// The kernel is bound by the W read-modify-write (8 B per element): shared memory goes to W
+// prefetch depth (WSLOTS x 16 KB in flight per SM) rather than to operand stages (K*P is small).
+constexpr int STAGES = POS_SFB_STAGES;   // operand ring depth
+constexpr int WSLOTS = POS_SFB_WSLOTS;   // W sub-tile ring depth
 constexpr int WSUB = 32;            // W sub-tile columns (32 fp32 = one 128-byte swizzle row)
 constexpr int NSUB = BN / WSUB;     // sub-tiles per tile
 constexpr int SWZ = 128;            // swizzle span in bytes (one operand "row" chunk)
-constexpr int A_BYTES = SWZ * BM;   // per stage: BK rows x BM elements = 128 B x BM (any dtype)
-constexpr int B_BYTES = SWZ * BN;
+#ifndef POS_SFB_KBYTES
+#define POS_SFB_KBYTES 128
+#endif
+constexpr int KBYTES = POS_SFB_KBYTES;   // bytes of K per operand row per stage (BK = KBYTES / elt)
+constexpr int A_BYTES = KBYTES * BM;     // per stage: BK rows x BM elements (any dtype)
+constexpr int B_BYTES = KBYTES * BN;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int W_BYTES = BM * WSUB * 4;
 constexpr int SMEM_DATA = STAGES * STAGE_BYTES + WSLOTS * W_BYTES;
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmW, TileInfo ti, float alpha, int accumulate) {
   constexpr int EB = kTF32 ? 4 : 2;          // element bytes
-  constexpr int BK = SWZ / EB;               // k rows per stage (64 bf16 / 32 tf32)
+  constexpr int BK = KBYTES / EB;            // k rows per stage (64 bf16 / 32 tf32 at 128 B)
   constexpr int CHUNK = SWZ / EB;            // elements per 128-byte chunk along m / n
   constexpr int UK = 32 / EB;                // UMMA K (16 bf16 / 8 tf32)
   constexpr int BOX_BYTES = BK * SWZ;        // one TMA box: BK rows x 128 B
@@ -404,7 +416,7 @@ template <bool kTF32>
 bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
                     int64_t ldw, int max_ctas) {
   constexpr int EB = kTF32 ? 4 : 2;
-  constexpr int BK = SWZ / EB, CHUNK = SWZ / EB;
+  constexpr int BK = KBYTES / EB, CHUNK = SWZ / EB;
   const int64_t R = row_elems(M, N), Mp = m_pad(M);
   const CUtensorMapDataType dt =
       kTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -435,6 +447,7 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
 
 template <bool kTF32>
 cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
+  clear_stale_launch_error();
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32>,

@@ -1,0 +1,325 @@
+// NVLink-SHARP / symmetric-memory path: the PS and SFB collectives fused into
+// the kernels that consume them, over NVSwitch multicast (NVLS) memory registered as NCCL symmetric
+// windows. NCCL provides only the plumbing (allocation, window registration, the device-side
+// pointers and the cross-GPU barrier); the data movement and arithmetic are these kernels.
+//
+//  * ps_nvls_kernel (A6 + A7 + A8 fused): rank r owns shard [lo, hi) of a dense unit.
+//      ghat = multimem.ld_reduce.add(grad[i])      -- the switch sums all P workers' gradients
+//      w    = W_local[i] + alpha * ghat            -- the server's "apply (+)"
+//      multimem.st(W[i], w)                        -- fresh parameters to every replica
+//    bracketed by two LSA barriers: gradients of all ranks complete before the reduce, every
+//    replica's W complete (and every gradient consumed) before any rank proceeds.
+//  * pack_mc_kernel (A2 + A3 fused): this rank's sufficient factors, packed and cast,
+//    are multicast-stored into its slot of EVERY rank's gather buffer (one NVLink egress copy; the
+//    switch replicates), followed by an LSA barrier so the reconstruction can read all P slots.
+//
+// All fused kernels of a context run on its comm stream, in the same order on every rank, so one
+// set of barrier indices [0, kBarriers) is reused sequentially (the session epochs persist in the
+// barrier resource buffer, also across CUDA-graph replays).
+#include <cuda_bf16.h>
+#include <nccl.h>
+#include <nccl_device.h>
+
+#include <vector>
+
+#include "ctx.h"
+
+namespace pos {
+
+constexpr int kBarriers = 64;   // max CTAs of a fused kernel
+
+struct SymmWindow {
+  char* base;
+  size_t bytes;
+  ncclWindow_t win;
+};
+
+struct SymmState {
+  ncclDevComm dev;
+  bool ready = false;
+  bool multimem = false;
+  std::vector<SymmWindow> windows;
+};
+
+static SymmState* state(pos_ctx* c) { return static_cast<SymmState*>(c->symm); }
+
+namespace {
+
+// ------------------------------------------------------------------------------ device -------
+__device__ __forceinline__ float4 mm_ld_reduce_v4(const float* p) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ float mm_ld_reduce(const float* p) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st_v4(float* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+constexpr int kPsThreads = 512;
+constexpr int kPsUnroll = 4;
+
+__global__ void __launch_bounds__(kPsThreads)
+ps_nvls_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, size_t off_w,
+               int64_t lo, int64_t hi, float alpha) {
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // every worker's gradient is in place
+  const float* gmc = static_cast<const float*>(ncclGetLsaMultimemPointer(wg, off_g, dc));
+  float* wmc = static_cast<float*>(ncclGetLsaMultimemPointer(ww, off_w, dc));
+  const float* wl = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
+  const int64_t v0 = lo / 4, v1 = hi / 4;   // lo is a multiple of 64
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kPsUnroll - 1) * stride < v1; i += kPsUnroll * stride) {
+    float4 g[kPsUnroll], w[kPsUnroll];
+#pragma unroll
+    for (int u = 0; u < kPsUnroll; ++u) {
+      g[u] = mm_ld_reduce_v4(gmc + 4 * (i + u * stride));
+      w[u] = *reinterpret_cast<const float4*>(wl + 4 * (i + u * stride));
+    }
+#pragma unroll
+    for (int u = 0; u < kPsUnroll; ++u) {
+      w[u].x = fmaf(alpha, g[u].x, w[u].x);
+      w[u].y = fmaf(alpha, g[u].y, w[u].y);
+      w[u].z = fmaf(alpha, g[u].z, w[u].z);
+      w[u].w = fmaf(alpha, g[u].w, w[u].w);
+      mm_st_v4(wmc + 4 * (i + u * stride), w[u]);
+    }
+  }
+  for (; i < v1; i += stride) {
+    float4 g = mm_ld_reduce_v4(gmc + 4 * i);
+    float4 w = *reinterpret_cast<const float4*>(wl + 4 * i);
+    w.x = fmaf(alpha, g.x, w.x);
+    w.y = fmaf(alpha, g.y, w.y);
+    w.z = fmaf(alpha, g.z, w.z);
+    w.w = fmaf(alpha, g.w, w.w);
+    mm_st_v4(wmc + 4 * i, w);
+  }
+  if (blockIdx.x == 0)   // scalar tail of the shard
+    for (int64_t j = v1 * 4 + threadIdx.x; j < hi; j += blockDim.x)
+      mm_st(wmc + j, fmaf(alpha, mm_ld_reduce(gmc + j), wl[j]));
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // every replica's W is complete
+}
+
+__device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float ld_in(const float* p) { return *p; }
+
+// One 16-byte output vector per thread iteration, multicast to every rank's gather buffer.
+template <typename Tin, bool kBF16>
+__global__ void __launch_bounds__(256)
+pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, const Tin* __restrict__ u,
+               const Tin* __restrict__ v, int64_t M, int64_t N, int64_t Mp, int64_t R,
+               int64_t K) {
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
+  float* dst = static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off_slot, dc));
+  constexpr int VEC = kBF16 ? 8 : 4;
+  const int64_t chunks_per_row = R / VEC, total = K * chunks_per_row;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = c / chunks_per_row, col = (c % chunks_per_row) * VEC;
+    const Tin* src;
+    int64_t idx, lim;
+    if (col < Mp) { src = u + k * M; idx = col; lim = M; }
+    else          { src = v + k * N; idx = col - Mp; lim = N; }
+    float4 o;
+    if constexpr (kBF16) {
+      __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) h[i] = __float2bfloat16_rn(idx + i < lim ? ld_in(src + idx + i) : 0.f);
+      o = *reinterpret_cast<const float4*>(h);   // bit pattern only; a store does not convert
+    } else {
+      o.x = idx + 0 < lim ? ld_in(src + idx + 0) : 0.f;
+      o.y = idx + 1 < lim ? ld_in(src + idx + 1) : 0.f;
+      o.z = idx + 2 < lim ? ld_in(src + idx + 2) : 0.f;
+      o.w = idx + 3 < lim ? ld_in(src + idx + 3) : 0.f;
+    }
+    // element offset of this 16-byte vector in float units: (k * R + col) * eb / 4
+    mm_st_v4(dst + ((k * R + col) * (kBF16 ? 2 : 4)) / 4, o);
+  }
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // all P slots have landed everywhere
+}
+
+int grid_for(int64_t items, int threads, int cap) {
+  int64_t g = (items + threads - 1) / threads;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------- host --------
+static int symm_init(pos_ctx* c) {
+  if (c->symm) return POS_OK;
+  POS_CHECK_ARG(c->comm, "symmetric memory needs a multi-rank context");
+  SymmState* st = new SymmState();
+  ncclDevCommRequirements reqs = {};
+  reqs.lsaMultimem = true;
+  reqs.lsaBarrierCount = kBarriers;
+  ncclResult_t r = ncclDevCommCreate(c->comm, &reqs, &st->dev);
+  if (r != ncclSuccess) {
+    delete st;
+    return ctx_nccl_fail(c, r, "ncclDevCommCreate(lsaMultimem)");
+  }
+  st->ready = true;
+  st->multimem = true;
+  c->symm = st;
+  return POS_OK;
+}
+
+void symm_destroy(pos_ctx* c) {
+  SymmState* st = state(c);
+  if (!st) return;
+  for (auto& w : st->windows) {
+    ncclCommWindowDeregister(c->comm, w.win);
+    ncclMemFree(w.base);
+  }
+  if (st->ready) ncclDevCommDestroy(c->comm, &st->dev);
+  delete st;
+  c->symm = nullptr;
+}
+
+bool symm_lookup(pos_ctx* c, const void* p, size_t bytes, ncclWindow_t* win, size_t* off) {
+  SymmState* st = state(c);
+  if (!st || !st->multimem) return false;
+  const char* q = static_cast<const char*>(p);
+  for (auto& w : st->windows)
+    if (q >= w.base && q + bytes <= w.base + w.bytes) {
+      *win = w.win;
+      *off = (size_t)(q - w.base);
+      return true;
+    }
+  return false;
+}
+
+int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
+                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done) {
+  clear_stale_launch_error();
+  *done = false;
+  const int P = c->world;
+  if (P < 2 || c->local) return POS_OK;
+  const int64_t padded = pos_padded_size(n, P);
+  ncclWindow_t wg, ww;
+  size_t og, ow;
+  if (!symm_lookup(c, grad, (size_t)padded * 4, &wg, &og) ||
+      !symm_lookup(c, W, (size_t)padded * 4, &ww, &ow) || (og % 16) || (ow % 16))
+    return POS_OK;   // not symmetric: caller uses the NCCL path
+  int64_t lo = 0, hi = 0;
+  pos_shard_range(n, P, c->rank, &lo, &hi);
+  if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
+  const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, 32);
+  ps_nvls_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_nvls_kernel launch");
+  if (ev_a1) POS_CUDA_TRY(record_timing_event(ev_a1, s));
+  *done = true;
+  return POS_OK;
+}
+
+int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
+                 const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done) {
+  clear_stale_launch_error();
+  *done = false;
+  if (c->world < 2 || c->local) return POS_OK;
+  const int64_t R = row_elems(M, N), eb = dtype_bytes(dtype);
+  const size_t slot_bytes = (size_t)(K * R * eb);
+  ncclWindow_t wgb;
+  size_t off;
+  if (!symm_lookup(c, gbuf, slot_bytes * c->world, &wgb, &off)) return POS_OK;
+  const size_t off_slot = off + (size_t)c->rank * slot_bytes;
+  const int vec = dtype == POS_DT_BF16 ? 8 : 4;
+  const int grid = grid_for(K * (R / vec), 256, kBarriers);
+  const int64_t Mp = m_pad(M);
+  const ncclDevComm& dc = state(c)->dev;
+  if (dtype == POS_DT_BF16) {
+    if (in_dtype == POS_IN_BF16)
+      pack_mc_kernel<__nv_bfloat16, true><<<grid, 256, 0, s>>>(
+          dc, wgb, off_slot, static_cast<const __nv_bfloat16*>(u),
+          static_cast<const __nv_bfloat16*>(v), M, N, Mp, R, K);
+    else
+      pack_mc_kernel<float, true><<<grid, 256, 0, s>>>(dc, wgb, off_slot,
+                                                        static_cast<const float*>(u),
+                                                        static_cast<const float*>(v), M, N, Mp, R, K);
+  } else {
+    if (in_dtype == POS_IN_BF16)
+      pack_mc_kernel<__nv_bfloat16, false><<<grid, 256, 0, s>>>(
+          dc, wgb, off_slot, static_cast<const __nv_bfloat16*>(u),
+          static_cast<const __nv_bfloat16*>(v), M, N, Mp, R, K);
+    else
+      pack_mc_kernel<float, false><<<grid, 256, 0, s>>>(dc, wgb, off_slot,
+                                                         static_cast<const float*>(u),
+                                                         static_cast<const float*>(v), M, N, Mp, R, K);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack_mc_kernel launch");
+  *done = true;
+  return POS_OK;
+}
+
+}  // namespace pos
+
+using namespace pos;
+
+extern "C" {
+
+int pos_mem_alloc(pos_ctx* c, int64_t bytes, void** out) {
+  clear_error();
+  POS_CHECK_ARG(c && out && bytes > 0, "bad arguments");
+  int rc = symm_init(c);
+  if (rc) return rc;
+  void* p = nullptr;
+  ncclResult_t r = ncclMemAlloc(&p, (size_t)bytes);
+  if (r != ncclSuccess) return ctx_nccl_fail(c, r, "ncclMemAlloc");
+  ncclWindow_t win;
+  r = ncclCommWindowRegister(c->comm, p, (size_t)bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    ncclMemFree(p);
+    return ctx_nccl_fail(c, r, "ncclCommWindowRegister");
+  }
+  state(c)->windows.push_back({static_cast<char*>(p), (size_t)bytes, win});
+  // NCCL's allocation/registration may leave a benign runtime error behind: consume it so it is
+  // not misreported by the next kernel-launch check
+  (void)cudaGetLastError();
+  cudaError_t e = cudaMemset(p, 0, (size_t)bytes);
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "cudaMemset(symmetric buffer)");
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "cudaDeviceSynchronize after pos_mem_alloc");
+  *out = p;
+  return POS_OK;
+}
+
+int pos_mem_free(pos_ctx* c, void* p) {
+  clear_error();
+  POS_CHECK_ARG(c && p, "bad arguments");
+  SymmState* st = state(c);
+  POS_CHECK_ARG(st, "no symmetric memory on this context");
+  for (size_t i = 0; i < st->windows.size(); ++i)
+    if (st->windows[i].base == p) {
+      cudaDeviceSynchronize();
+      ncclCommWindowDeregister(c->comm, st->windows[i].win);
+      ncclMemFree(p);
+      st->windows.erase(st->windows.begin() + i);
+      return POS_OK;
+    }
+  POS_FAIL(POS_EINVAL, "pointer was not allocated by pos_mem_alloc");
+}
+
+int pos_mem_is_symmetric(pos_ctx* c, const void* p, int64_t bytes) {
+  ncclWindow_t w;
+  size_t off;
+  return (c && symm_lookup(c, p, (size_t)bytes, &w, &off)) ? 1 : 0;
+}
+
+}  // extern "C"

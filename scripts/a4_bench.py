@@ -1,0 +1,27 @@
+"""Isolated timing of the A4 reconstruct-and-apply kernel (pos_reconstruct_apply) on the bench
+shapes: CUDA events around each launch on its stream, inputs larger than L2 rotated between
+launches. Prints algorithmic GB/s (8MN + 2KP(M+N)) and fraction of the measured HBM peak."""
+import json, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1706_03292_b200 as pos
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+shapes = [(4096, 25088, 32), (21841, 4096, 32), (4096, 4096, 32), (4096, 25088, 256), (21841, 4096, 256), (4096, 9216, 1024)]
+tag = os.environ.get("TAG", os.path.basename(pos.LIB_PATH))
+for (M, N, KP) in shapes:
+    R = pos.pos_factor_row_elems(M, N)
+    G = (torch.randn(KP, R, device="cuda") * 0.03).to(torch.bfloat16)
+    nrot = 3
+    Ws = [torch.randn(M, N, device="cuda") for _ in range(nrot)]
+    for i in range(3):
+        pos.pos_reconstruct_apply(M, N, KP, pos.POS_DT_BF16, G, Ws[i % nrot], None, -1e-3)
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(12):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(); pos.pos_reconstruct_apply(M, N, KP, pos.POS_DT_BF16, G, Ws[i % nrot], None, -1e-3); e1.record()
+        torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+    ts.sort(); t = ts[len(ts) // 2] * 1e-3
+    byts = 8 * M * N + 2 * KP * (M + N)
+    print(json.dumps({"tag": tag, "M": M, "N": N, "KP": KP, "us": round(t * 1e6, 1), "GBs": round(byts / t / 1e9), "frac": round(byts / t / 1e9 / peak, 3),
+                      "tflops": round(2 * M * N * KP / t / 1e12, 1)}), flush=True)

@@ -82,6 +82,29 @@ def _worker(rank, world, port, outdir):
         torch.cuda.synchronize()
         check("ps_exact", np.array_equal(to_host(Wd[:n]), sync.ps_update(w0, gs, a)))
         res["digests"]["ps"] = _digest(Wd[:n])
+        # ---- (b2) PS through the fused NVLS kernel (grad and W in symmetric memory) -------------
+        Ws = ctx.sym_empty(Pn)
+        Gs = ctx.sym_empty(Pn)
+        check("symm_alloc", ctx.is_symmetric(Ws) and ctx.is_symmetric(Gs) and not ctx.is_symmetric(Wd))
+        Ws[:n] = to_dev(w0)
+        Gs[:n] = to_dev(gs[rank])
+        torch.cuda.synchronize()
+        ctx.sync_layer_ps(n, Gs, Ws, a)
+        torch.cuda.synchronize()
+        check("ps_nvls_exact", np.array_equal(to_host(Ws[:n]), sync.ps_update(w0, gs, a)))
+        res["digests"]["ps_nvls"] = _digest(Ws[:n])
+        # odd sizes: shard tails, tiny layers with empty shards
+        for n_odd in (1, 10, 4097, 1792 + 36928):
+            P_o = pos.pos_padded_size(n_odd, P)
+            go = [si.exact_dense_grad(si.rng(48, n_odd % 97, p), n_odd) for p in range(P)]
+            wo = si.exact_weights(si.rng(48, 1), n_odd)
+            Wo, Go = ctx.sym_empty(P_o), ctx.sym_empty(P_o)
+            Wo[:n_odd] = to_dev(wo)
+            Go[:n_odd] = to_dev(go[rank])
+            torch.cuda.synchronize()
+            ctx.sync_layer_ps(n_odd, Go, Wo, a)
+            torch.cuda.synchronize()
+            check(f"ps_nvls_exact_{n_odd}", np.array_equal(to_host(Wo[:n_odd]), sync.ps_update(wo, go, a)))
         # ---- (c) FC forced onto the PS path == SFB result ------------------------------------
         M2, N2, K2 = 1000, 4100, 8
         Us2, Vs2 = zip(*(si.exact_factors(si.rng(42, 0, p), K2, M2, N2) for p in range(P)))
@@ -111,22 +134,23 @@ def _worker(rank, world, port, outdir):
         check("sfb_stat_dW", err(g3 - W30, Wr3 - W30) <= 2e-3)
         res["digests"]["sfb_stat"] = _digest(W3)
         # ---- (e) WFBP scheduler: FC (SFB) + bucket + dense; WFBP == sequential, both == oracle --
-        def run_sched(sequential, graph):
+        def run_sched(sequential, graph, symm_dense=False):
+            alloc = (lambda k: ctx.sym_empty(k)) if symm_dense else (lambda k: torch.zeros(k, device=dev))
             sch = pos.Scheduler(ctx, 5, timing="apply", sequential=sequential)
             sizes = [1792, 36928]
             nb = sum(sizes)
             Pb = pos.pos_padded_size(nb, P)
             wb0 = si.exact_weights(si.rng(44, 0), nb)
             gb = [si.exact_dense_grad(si.rng(44, 1, p), nb) for p in range(P)]
-            Wb = torch.zeros(Pb, device=dev); Wb[:nb] = to_dev(wb0)
-            Gb = torch.zeros(Pb, device=dev)
+            Wb = alloc(Pb); Wb[:nb] = to_dev(wb0)
+            Gb = alloc(Pb)
             sch.add_dense_bucket(0, sizes, Wb, Gb)
             n2 = 590080
             Pd = pos.pos_padded_size(n2, P)
             wd0 = si.exact_weights(si.rng(45, 0), n2)
             gd = [si.exact_dense_grad(si.rng(45, 1, p), n2) for p in range(P)]
-            Wq = torch.zeros(Pd, device=dev); Wq[:n2] = to_dev(wd0)
-            Gq = torch.zeros(Pd, device=dev)
+            Wq = alloc(Pd); Wq[:n2] = to_dev(wd0)
+            Gq = alloc(Pd)
             sch.add_dense(2, n2, Wq, Gq)
             Mf, Nf, Kf = 4096, 9216, 16
             Uf, Vf = zip(*(si.exact_factors(si.rng(46, 0, p), Kf, Mf, Nf) for p in range(P)))
@@ -180,10 +204,15 @@ def _worker(rank, world, port, outdir):
         ok_w, dig_w = run_sched(False, False)
         ok_s, dig_s = run_sched(True, False)
         ok_g, dig_g = run_sched(False, True)
+        ok_n, dig_n = run_sched(False, True, symm_dense=True)
+        ok_ns, dig_ns = run_sched(True, False, symm_dense=True)
+        check("sched_nvls_graph_oracle", ok_n)
+        check("sched_nvls_seq_oracle", ok_ns)
         check("sched_wfbp_oracle", ok_w)
         check("sched_seq_oracle", ok_s)
         check("sched_graph_oracle", ok_g)
         check("sched_wfbp_eq_seq", dig_w == dig_s == dig_g)
+        check("sched_nvls_eq_nccl", dig_n == dig_ns == dig_w)
         res["digests"]["sched"] = dig_w
         ctx.close()
     except Exception as e:  # report, do not hang the other ranks silently
