@@ -154,7 +154,9 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
   }
   // stream of the first stage: the comm stream when a collective follows, else an apply stream
   cudaStream_t as = un.scheme == POS_SCHEME_SFB ? s->pool[0] : s->pool[1 + un.seq % (kPool - 1)];
-  cudaStream_t cs = coll ? c->comm_stream : as;
+  // first stage: the comm stream when a collective follows; else an auxiliary apply stream, so the
+  // factor pack of the next SFB layer overlaps the reconstruction of this one
+  cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % (kPool - 1)];
   for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_ready, 0));
   if (s->flags & POS_SCHED_SEQUENTIAL) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_end, 0));
   if (ts && (rc = trec(ts->start, cs))) return rc;
@@ -186,8 +188,10 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
       if (ts && (rc = trec(ts->gathered, cs))) return rc;
       POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));   // sync events last: joins a capture
       POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
-    } else if (ts && (rc = trec(ts->gathered, cs))) {
-      return rc;
+    } else {
+      if (ts && (rc = trec(ts->gathered, cs))) return rc;
+      POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));
+      POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
     }
     // Move(CPU2GPU) analogue: A4 + A4b on the apply stream
     if (ts && (rc = trec(ts->a0, as))) return rc;

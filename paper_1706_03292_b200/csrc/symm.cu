@@ -20,13 +20,14 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.h"
 
 namespace pos {
 
-constexpr int kBarriers = 64;   // max CTAs of a fused kernel
+constexpr int kBarriers = 128;  // max CTAs of a fused kernel
 
 struct SymmWindow {
   char* base;
@@ -123,6 +124,10 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, const Tin* __r
                const Tin* __restrict__ v, int64_t M, int64_t N, int64_t Mp, int64_t R,
                int64_t K) {
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
+  // Entry barrier: every rank has reached this iteration's pack on its comm stream, which (by
+  // pos_sched_end's contract) is after its previous reconstruction finished reading the gather
+  // buffer we are about to overwrite (cross-rank WAR).
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   float* dst = static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off_slot, dc));
   constexpr int VEC = kBF16 ? 8 : 4;
   const int64_t chunks_per_row = R / VEC, total = K * chunks_per_row;
@@ -174,6 +179,9 @@ static int symm_init(pos_ctx* c) {
     return ctx_nccl_fail(c, r, "ncclDevCommCreate(lsaMultimem)");
   }
   st->ready = true;
+  // with the collectives fused into our own kernels (which co-reside with the reconstruction
+  // kernel) no SMs need to be kept free for NCCL CTAs
+  if (!getenv("POS_SFB_MAX_CTAS")) c->max_ctas = 0;
   st->multimem = true;
   c->symm = st;
   return POS_OK;
@@ -219,7 +227,13 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   int64_t lo = 0, hi = 0;
   pos_shard_range(n, P, c->rank, &lo, &hi);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
-  const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, 32);
+  // NVLS loads have microsecond latency: keep ~2 MB of reductions in flight per GPU
+  static const int ps_ctas = [] {
+    const char* e = getenv("POS_NVLS_CTAS");
+    const int v = (e && *e) ? atoi(e) : 96;
+    return v < 1 ? 1 : (v > kBarriers ? kBarriers : v);
+  }();
+  const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, ps_ctas);
   ps_nvls_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_nvls_kernel launch");
