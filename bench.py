@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "tf32", "f32"])
     ap.add_argument("--sequential", action="store_true", help="WFBP off: sync after the whole step")
     ap.add_argument("--max-ctas", type=int, default=0)
-    ap.add_argument("--bucket-mb", type=float, default=2.0,
+    ap.add_argument("--bucket-mb", type=float, default=16.0,
                     help="PS unit = consecutive dense layers up to this many MiB of fp32 (the paper's "
                          "2 MB KV pairs); 0 = one unit per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")

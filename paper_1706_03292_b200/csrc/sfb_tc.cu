@@ -31,7 +31,10 @@ namespace pos {
 namespace {
 
 constexpr int BM = 128;             // tile rows (m) = UMMA M = TMEM lanes
-constexpr int BN = 256;             // tile cols (n) = UMMA N = TMEM columns per accumulator
+#ifndef POS_SFB_BN
+#define POS_SFB_BN 256
+#endif
+constexpr int BN = POS_SFB_BN;      // tile cols (n) = UMMA N = TMEM columns per accumulator
 #ifndef POS_SFB_STAGES
 #define POS_SFB_STAGES 3
 #endif

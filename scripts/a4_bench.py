@@ -25,3 +25,21 @@ for (M, N, KP) in shapes:
     byts = 8 * M * N + 2 * KP * (M + N)
     print(json.dumps({"tag": tag, "M": M, "N": N, "KP": KP, "us": round(t * 1e6, 1), "GBs": round(byts / t / 1e9), "frac": round(byts / t / 1e9 / peak, 3),
                       "tflops": round(2 * M * N * KP / t / 1e12, 1)}), flush=True)
+# streaming reference: A7 shard apply (read g, read W, write W) over 100M elements
+n = 100 * 2**20
+g = torch.randn(n, device="cuda"); Wx = [torch.randn(n, device="cuda") for _ in range(2)]
+for i in range(3): pos.pos_ps_apply(g, Wx[i % 2], n, -1e-3)
+torch.cuda.synchronize(); ts = []
+for i in range(10):
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record(); pos.pos_ps_apply(g, Wx[i % 2], n, -1e-3); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+ts.sort(); t = ts[5] * 1e-3
+print(json.dumps({"tag": tag, "M": 0, "N": n, "KP": 0, "us": round(t * 1e6, 1), "GBs": round(12 * n / t / 1e9), "frac": round(12 * n / t / 1e9 / peak, 3), "tflops": 0}), flush=True)
+# copy reference (torch): read + write
+for i in range(3): Wx[0].copy_(Wx[1])
+torch.cuda.synchronize(); ts = []
+for i in range(10):
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record(); Wx[i % 2].copy_(Wx[(i + 1) % 2]); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+ts.sort(); t = ts[5] * 1e-3
+print(json.dumps({"tag": tag, "M": 1, "N": n, "KP": 0, "us": round(t * 1e6, 1), "GBs": round(8 * n / t / 1e9), "frac": round(8 * n / t / 1e9 / peak, 3), "tflops": 0}), flush=True)
