@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-symm", action="store_true",
                     help="P > 1: keep PS buffers and SFB gather buffers out of symmetric (NVLS) memory, i.e. use the stock NCCL collectives")
+    ap.add_argument("--static-tiles", action="store_true", help="static round-robin reconstruction tiles")
+    ap.add_argument("--ps-after-sfb", action="store_true",
+                    help="P > 1: PS units wait for the SFB reconstructions instead of overlapping them")
     ap.add_argument("--eager", action="store_true",
                     help="issue every step from the host (default: replay the step as a CUDA graph)")
     ap.add_argument("--layers", action="store_true", help="also print a per-layer table to stderr")
@@ -250,7 +253,7 @@ def run_ours(a):
     gen.manual_seed(1000 * 1 + rank)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
     sch = pos.Scheduler(ctx, L, timing=("apply" if not a.layers else True), sequential=a.sequential,
-                        symm=not a.no_symm)
+                        symm=not a.no_symm, ps_after_sfb=a.ps_after_sfb, static_tiles=a.static_tiles)
     bufs = [None] * L
     for un in units:
         if un["kind"] == "fc":

@@ -61,7 +61,11 @@ enum {
  * TIMING_APPLY = only the apply stage (reconstruct-and-apply, shard apply) is bracketed, which
  * adds the fewest graph nodes; SEQUENTIAL = WFBP off (sync after the whole backward). */
 enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2, POS_SCHED_TIMING_APPLY = 4,
-       POS_SCHED_NO_SYMM = 8 /* keep SFB gather buffers out of symmetric memory (NCCL path) */ };
+       POS_SCHED_NO_SYMM = 8 /* keep SFB gather buffers out of symmetric memory (NCCL path) */,
+       POS_SCHED_PS_AFTER_SFB = 16 /* P > 1: a dense unit's sync waits for the previously issued
+                                      SFB reconstruction instead of overlapping it */,
+       POS_SCHED_STATIC_TILES = 32 /* reconstruction tiles in static round-robin order instead of
+                                      the dynamic (atomic-counter) tile scheduler */ };
 
 /* ABI version (major * 100 + minor). */
 int pos_version(void);

@@ -19,7 +19,8 @@ POS_ROLE_SERVER, POS_ROLE_WORKER, POS_ROLE_BOTH = 0, 1, 2
 POS_DT_BF16, POS_DT_TF32, POS_DT_F32 = 0, 1, 2
 POS_IN_BF16, POS_IN_F32 = 0, 1
 POS_OK, POS_EINVAL, POS_ESTATE, POS_ECUDA, POS_ENCCL, POS_ENOMEM, POS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY, POS_SCHED_NO_SYMM = 1, 2, 4, 8
+POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY, POS_SCHED_NO_SYMM, POS_SCHED_PS_AFTER_SFB = 1, 2, 4, 8, 16
+POS_SCHED_STATIC_TILES = 32
 
 DTYPES = {"bf16": POS_DT_BF16, "tf32": POS_DT_TF32, "f32": POS_DT_F32}
 SCHEME_NAMES = {POS_SCHEME_PS: "PS", POS_SCHEME_SFB: "SFB", POS_SCHEME_ADAM: "ADAM"}
@@ -239,13 +240,15 @@ class Context:
 class Scheduler:
     """pos_sched: WFBP per-layer scheduler (Algorithm 2 on CUDA streams/events)."""
 
-    def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False, symm=True):
+    def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False, symm=True,
+                 ps_after_sfb=False, static_tiles=False):
         """timing: False | True (all stages) | "apply" (apply stage only). symm: place SFB gather
         buffers in symmetric memory (multicast factor pack) when world > 1."""
         self.ctx = ctx
         h = C.c_void_p()
         tflag = POS_SCHED_TIMING_APPLY if timing == "apply" else (POS_SCHED_TIMING if timing else 0)
-        flags = tflag | (POS_SCHED_SEQUENTIAL if sequential else 0) | (0 if symm else POS_SCHED_NO_SYMM)
+        flags = (tflag | (POS_SCHED_SEQUENTIAL if sequential else 0) | (0 if symm else POS_SCHED_NO_SYMM)
+                 | (POS_SCHED_PS_AFTER_SFB if ps_after_sfb else 0) | (POS_SCHED_STATIC_TILES if static_tiles else 0))
         _chk(lib().pos_sched_create(ctx.h, n_layers, flags, C.byref(h)), "pos_sched_create")
         self.h = h
         self.L = n_layers

@@ -93,6 +93,9 @@ struct SfbTcPlan {
   int64_t M = 0, N = 0, KP = 0;
   int nb_n = 0, num_tiles = 0, nkb = 0, grid = 0;
   bool tf32 = false;
+  // device scratch (2 x u32, zero-initialised, owned by the plan's creator) for the dynamic tile
+  // scheduler; nullptr = static round-robin tiles. Launches sharing a counter must not overlap.
+  unsigned int* counter = nullptr;
 };
 // false if the shape/alignment/dtype cannot use the tensor-core kernel
 bool sfb_tc_make_plan(SfbTcPlan* plan, int64_t M, int64_t N, int64_t KP, int32_t dtype,

@@ -50,6 +50,7 @@ struct Unit {
   pos::SfbTcPlan plan;         // cached TMA descriptors of the tensor-core reconstruction
   bool has_plan = false;
   int plan_ctas = -1;
+  unsigned int* tile_counter = nullptr;   // dynamic tile scheduler state of this unit's launches
   std::vector<int> members;    // layer indices (forward order)
   int pending = 0;             // members not yet triggered in this iteration
   const void* u = nullptr;     // FC factors of this iteration
@@ -85,6 +86,8 @@ struct pos_sched {
   cudaEvent_t ev_end = nullptr;
   int64_t iter = 0;        // iterations begun
   bool captured = false;   // some iteration was issued under CUDA-graph stream capture
+  int last_sfb = -1;       // most recently issued SFB unit of this iteration
+  bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
 };
 
 using namespace pos;
@@ -158,6 +161,11 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
   // factor pack of the next SFB layer overlaps the reconstruction of this one
   cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % (kPool - 1)];
   for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_ready, 0));
+  // Optionally keep the NVLink-latency-bound PS kernels from co-running with the HBM-bound
+  // reconstructions (they starve each other's memory pipelines); see DESIGN.md.
+  if (coll && s->ps_after_sfb && un.scheme != POS_SCHEME_SFB && s->last_sfb >= 0)
+    POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->units[s->last_sfb].ev_done, 0));
+  if (un.scheme == POS_SCHEME_SFB) s->last_sfb = ui;
   if (s->flags & POS_SCHED_SEQUENTIAL) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_end, 0));
   if (ts && (rc = trec(ts->start, cs))) return rc;
   if (un.scheme == POS_SCHEME_SFB) {
@@ -198,6 +206,7 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
     if (un.plan_ctas != c->max_ctas) {   // (re)build the cached launch plan
       un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * P, un.dtype, un.gbuf, un.W,
                                      un.N, c->max_ctas);
+      un.plan.counter = (s->flags & POS_SCHED_STATIC_TILES) ? nullptr : un.tile_counter;
       un.plan_ctas = c->max_ctas;
     }
     if (un.has_plan) {
@@ -296,13 +305,15 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   POS_CHECK_ARG(c && out, "NULL argument");
   POS_CHECK_ARG(n_layers >= 1, "n_layers must be >= 1");
   POS_CHECK_ARG((flags & ~(POS_SCHED_TIMING | POS_SCHED_SEQUENTIAL | POS_SCHED_TIMING_APPLY |
-                            POS_SCHED_NO_SYMM)) == 0,
+                            POS_SCHED_NO_SYMM | POS_SCHED_PS_AFTER_SFB |
+                            POS_SCHED_STATIC_TILES)) == 0,
                 "unknown flags");
   POS_CHECK_ARG(!c->local || c->world == 1, "the scheduler needs a real (or 1-worker) context");
   pos_sched* s = new pos_sched();
   s->ctx = c;
   s->L = n_layers;
   s->flags = flags;
+  s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
   int lo = 0, hi = 0;
@@ -360,6 +371,10 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
     cudaError_t e = cudaMalloc(&u.gbuf, bytes);
     if (e != cudaSuccess) { (void)cudaGetLastError(); POS_FAIL(POS_ENOMEM, "cudaMalloc(%zu)", bytes); }
   }
+  if (scheme == POS_SCHEME_SFB) {   // all launches of this unit run on one stream, in order
+    POS_CUDA_TRY(cudaMalloc(&u.tile_counter, 2 * sizeof(unsigned int)));
+    POS_CUDA_TRY(cudaMemset(u.tile_counter, 0, 2 * sizeof(unsigned int)));
+  }
   if (scheme == POS_SCHEME_PS) {
     const int64_t padded = pos_padded_size(n, c->world);
     if (padded > n) POS_CUDA_TRY(cudaMemset(grad + n, 0, (size_t)(padded - n) * sizeof(float)));
@@ -413,6 +428,7 @@ int pos_sched_begin(pos_sched* s, float alpha) {
   for (auto& un : s->units) un.pending = (int)un.members.size();
   s->order.clear();
   s->n_triggered = 0;
+  s->last_sfb = -1;
   s->alpha = alpha;
   s->in_iter = true;
   s->iter += 1;
@@ -539,6 +555,7 @@ int pos_sched_destroy(pos_sched* s) {
       if (un.gbuf_symm) pos_mem_free(s->ctx, un.gbuf);
       else cudaFree(un.gbuf);
     }
+    if (un.tile_counter) cudaFree(un.tile_counter);
   }
   for (auto& ly : s->layers)
     if (ly.ev_ready) cudaEventDestroy(ly.ev_ready);

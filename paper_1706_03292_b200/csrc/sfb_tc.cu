@@ -57,7 +57,8 @@ constexpr int B_BYTES = KBYTES * BN;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int W_BYTES = BM * WSUB * 4;
 constexpr int SMEM_DATA = STAGES * STAGE_BYTES + WSLOTS * W_BYTES;
-constexpr int SMEM_BARS = 8 * (2 * STAGES + 2 * WSLOTS + 4) + 16;
+constexpr int TR = 4;               // tile-index ring depth (dynamic tile scheduler)
+constexpr int SMEM_BARS = 8 * (2 * STAGES + 2 * WSLOTS + 4 + 2 * TR) + 16 + 4 * TR;
 constexpr int SMEM_TOTAL = SMEM_DATA + SMEM_BARS + 1024;   // + alignment slack
 constexpr int THREADS = 256;
 constexpr int TMEM_COLS = 2 * BN;
@@ -196,6 +197,10 @@ struct TileInfo {
   int nb_n;        // tiles along n
   int num_tiles;
   int nkb;         // k blocks
+  // Dynamic tile scheduler: [0] = next tile, [1] = CTAs finished. nullptr = static round-robin.
+  // Self-resetting: the last CTA to finish zeroes both, so the counter is reusable by the next
+  // launch on the same stream (and by every CUDA-graph replay).
+  unsigned int* counter;
 };
 
 template <bool kTF32>
@@ -218,7 +223,24 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const uint32_t b_full = smem_u32(bars), b_empty = b_full + 8 * STAGES;
   const uint32_t b_wfull = b_empty + 8 * STAGES, b_wempty = b_wfull + 8 * WSLOTS;
   const uint32_t b_tfull = b_wempty + 8 * WSLOTS, b_tempty = b_tfull + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * WSLOTS + 4);
+  const uint32_t b_rfull = b_tempty + 16, b_rempty = b_rfull + 8 * TR;   // tile-index ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 * WSLOTS + 4 + 2 * TR);
+  volatile int* tile_ring = reinterpret_cast<volatile int*>(tmem_slot + 4);
+  const bool dyn = ti.counter != nullptr;
+  // The tile sequence every role walks: static round-robin, or the fetcher's atomic sequence
+  // broadcast through the ring (it -> tile, -1 = done). All roles see the same sequence.
+  auto tile_of = [&](int it, uint32_t& rphase) -> int {
+    if (!dyn) {
+      const int t = blockIdx.x + it * gridDim.x;
+      return t < ti.num_tiles ? t : -1;
+    }
+    const int slot = it % TR;
+    mbar_wait(b_rfull + 8 * slot, rphase);
+    const int t = tile_ring[slot];
+    mbar_arrive(b_rempty + 8 * slot);
+    if (slot == TR - 1) rphase ^= 1;
+    return t;
+  };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -226,6 +248,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     for (int i = 0; i < STAGES; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, 1); }
     for (int i = 0; i < WSLOTS; ++i) { mbar_init(b_wfull + 8 * i, 1); mbar_init(b_wempty + 8 * i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(b_tfull + 8 * i, 1); mbar_init(b_tempty + 8 * i, 128); }
+    // ring consumers: MMA issuer + W producer + 128 epilogue threads
+    for (int i = 0; i < TR; ++i) { mbar_init(b_rfull + 8 * i, 1); mbar_init(b_rempty + 8 * i, 130); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -249,8 +273,30 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     // ===================== operand TMA producer =====================
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+      uint32_t phase = 0, rphase = 0;
+      for (int it = 0;; ++it) {
+        int t;
+        if (!dyn) {
+          t = blockIdx.x + it * gridDim.x;
+          if (t >= ti.num_tiles) break;
+        } else {   // fetch the next tile and publish it to the other roles
+          const int slot = it % TR;
+          mbar_wait(b_rempty + 8 * slot, rphase ^ 1);
+          t = (int)atomicAdd(ti.counter, 1u);
+          if (t >= ti.num_tiles) t = -1;
+          tile_ring[slot] = t;
+          mbar_arrive(b_rfull + 8 * slot);
+          if (slot == TR - 1) rphase ^= 1;
+          if (t < 0) {
+            __threadfence();
+            if (atomicAdd(ti.counter + 1, 1u) == gridDim.x - 1) {   // last CTA out resets
+              ti.counter[0] = 0;
+              ti.counter[1] = 0;
+              __threadfence();
+            }
+            break;
+          }
+        }
         const int m0 = (t / ti.nb_n) * BM, n0 = (t % ti.nb_n) * BN;
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(b_empty + 8 * stage, phase ^ 1);
@@ -272,8 +318,10 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
-      uint32_t aphase = 0;
-      for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+      uint32_t aphase = 0, rphase = 0;
+      for (int it = 0;; ++it) {
+        const int t = tile_of(it, rphase);
+        if (t < 0) break;
         mbar_wait(b_tempty + 8 * acc, aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -298,8 +346,10 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     // ===================== W sub-tile TMA producer =====================
     if (lane == 0) {
       int ws = 0;
-      uint32_t wphase = 0;
-      for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+      uint32_t wphase = 0, rphase = 0;
+      for (int it = 0;; ++it) {
+        const int t = tile_of(it, rphase);
+        if (t < 0) break;
         const int m0 = (t / ti.nb_n) * BM, n0 = (t % ti.nb_n) * BN;
         const int nsub = nsub_of(ti.N, n0);
         for (int j = 0; j < nsub; ++j) {
@@ -325,7 +375,10 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     int ws = 0;
     uint32_t wphase = 0;
     int pending = -1;                         // slot whose TMA store has not been retired yet
-    for (int t = blockIdx.x; t < ti.num_tiles; t += gridDim.x) {
+    uint32_t rphase = 0;
+    for (int it = 0;; ++it) {
+      const int t = tile_of(it, rphase);
+      if (t < 0) break;
       const int m0 = (t / ti.nb_n) * BM, n0 = (t % ti.nb_n) * BN;
       const int nsub = nsub_of(ti.N, n0);
       mbar_wait(b_tfull + 8 * acc, aphase);
@@ -461,6 +514,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   TileInfo ti;
   ti.M = pl.M; ti.N = pl.N; ti.KP = pl.KP;
   ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
+  ti.counter = pl.counter;
   sfb_tc_kernel<kTF32><<<pl.grid, THREADS, SMEM_TOTAL, s>>>(pl.tmA, pl.tmB, pl.tmW, ti, alpha,
                                                               accumulate);
   return cudaGetLastError();

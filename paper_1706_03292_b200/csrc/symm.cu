@@ -230,7 +230,7 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   // NVLS loads have microsecond latency: keep ~2 MB of reductions in flight per GPU
   static const int ps_ctas = [] {
     const char* e = getenv("POS_NVLS_CTAS");
-    const int v = (e && *e) ? atoi(e) : 96;
+    const int v = (e && *e) ? atoi(e) : 32;
     return v < 1 ? 1 : (v > kBarriers ? kBarriers : v);
   }();
   const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, ps_ctas);

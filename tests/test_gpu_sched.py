@@ -45,9 +45,9 @@ def oracle_result(model, alpha):
     return res
 
 
-def run(model, alpha, sequential=False, timing=False, delay_cycles=0):
+def run(model, alpha, sequential=False, timing=False, delay_cycles=0, static_tiles=False):
     ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
-    sch = pos.Scheduler(ctx, len(model), timing=timing, sequential=sequential)
+    sch = pos.Scheduler(ctx, len(model), timing=timing, sequential=sequential, static_tiles=static_tiles)
     dev = []
     for l, d in enumerate(model):
         if d["kind"] == "dense":
@@ -292,3 +292,35 @@ def test_sched_dense_bucket(timing):
         assert sch.timing(0)[2] > 0
     sch.close()
     ctx.close()
+
+
+def test_sched_dynamic_tiles_bitwise_equal_static_and_repeatable():
+    """The dynamic tile scheduler (atomic tile fetch, self-resetting counter) changes which CTA
+    computes a tile, never the tile's arithmetic: bitwise equal to the static order, over repeated
+    iterations (the counter must reset after every launch)."""
+    model = make_model(5)
+    a = si.EXACT_ALPHA
+    dyn, _, _ = run(model, a)
+    sta, _, _ = run(model, a, static_tiles=True)
+    for (Wd, bd), (Ws, bs) in zip(dyn, sta):
+        assert np.array_equal(Wd, Ws)
+    # statistical regime, several iterations: dynamic == static bit for bit
+    M, N, K = 4096, 25088, 32
+    res = []
+    for static in (False, True):
+        ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+        sch = pos.Scheduler(ctx, 1, static_tiles=static)
+        g = si.rng(60)
+        u, v = si.stat_factors(g, K, M, N, "bf16")
+        W = to_dev(si.stat_weights(si.rng(61), M, N))
+        sch.add_fc(0, M, N, K, W, None, None, "bf16", pos.POS_IN_BF16)
+        ud, vd = to_dev(u, "bf16"), to_dev(v, "bf16")
+        for _ in range(5):
+            sch.begin(-0.01)
+            sch.factors_ready(0, ud, vd)
+            sch.end()
+        torch.cuda.synchronize()
+        res.append(W.cpu().numpy())
+        sch.close()
+        ctx.close()
+    assert np.array_equal(res[0], res[1])
