@@ -159,7 +159,7 @@ int pos_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t 
  *   b[m]    = (accumulate ? b[m]    : 0) + alpha * sum_{j < KP} U[j][m]        (if b != NULL)
  * where row j of the gathered buffer G (KP rows of pos_factor_row_elems(M,N) elements, packed by
  * pos_pack_factors, worker-major: j = p*K + k) holds [u_j | v_j]. W: device fp32, row stride ldw
- * elements (ldw >= N). BF16/TF32 run the tcgen05/TMEM/TMA kernel when ldw % 4 == 0 and W is
+ * elements (ldw >= N). BF16/TF32 run the tcgen05/TMEM/TMA kernel when N % 4 == 0, ldw % 4 == 0 and W is
  * 16-byte aligned (else the SIMT kernel); F32 always runs the exact SIMT FFMA kernel. The k order
  * is fixed, so results are bitwise reproducible. */
 int pos_reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,

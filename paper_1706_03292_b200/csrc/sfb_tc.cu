@@ -523,7 +523,10 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
 }  // namespace
 
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
-  return (ldw % 4) == 0 && aligned16(W) && aligned16(G) && N >= 1 && get_encode() != nullptr;
+  // TMA stores move whole 16-byte chunks: the last W row chunk must not straddle column N (else
+  // the element(s) after N in a strided W would be overwritten) -> N % 4 == 0 as well as ldw.
+  return (N % 4) == 0 && (ldw % 4) == 0 && aligned16(W) && aligned16(G) && N >= 1 &&
+         get_encode() != nullptr;
 }
 
 bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t dtype,
