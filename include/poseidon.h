@@ -101,7 +101,9 @@ int pos_shard_range(int64_t n, int32_t P, int32_t r, int64_t* begin, int64_t* en
 /* Elements a caller must allocate for a PS layer's W and grad buffers: P * S. */
 int64_t pos_padded_size(int64_t n, int32_t P);
 /* Row length (elements) of the library's gathered factor layout for an FC layer:
- * M_pad + N_pad with M_pad = ceil(M/8)*8, N_pad = ceil(N/8)*8 (16-byte TMA row rule). */
+ * M_pad + N_pad with M_pad = ceil(M/8)*8, N_pad = ceil((N+1)/8)*8 (16-byte TMA row rule; column N
+ * of the v part is the "ones column" that makes the reconstruction GEMM also produce the bias
+ * gradient sum_j u_j, reading S12). */
 int64_t pos_factor_row_elems(int64_t M, int64_t N);
 
 /* ======================================================================================
@@ -148,7 +150,7 @@ int pos_set_max_ctas(pos_ctx* ctx, int32_t max_ctas);
 
 /* A2 — SFB factor pack ("transformation between SFs and gradients"): write the K rows
  *   slot[k][0 .. M_pad)            = dtype(u[k][0..M)), zero in [M, M_pad)
- *   slot[k][M_pad .. M_pad+N_pad)  = dtype(v[k][0..N)), zero in the pad
+ *   slot[k][M_pad .. M_pad+N_pad)  = dtype(v[k][0..N)), 1.0 at M_pad+N (ones column), zero after
  * slot: device, K * pos_factor_row_elems(M,N) elements of bf16 (dtype BF16) or fp32 (TF32/F32),
  * 16-byte aligned. u, v: device, in_dtype storage, any alignment. */
 int pos_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,

@@ -43,7 +43,8 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 // gathered factor row layout: [u (M_pad) | v (N_pad)], pads of 8 elements (16 B for bf16)
 inline int64_t m_pad(int64_t M) { return round_up(M, 8); }
-inline int64_t n_pad(int64_t N) { return round_up(N, 8); }
+// N_pad >= N + 1: column N of every v row is the 1.0 "ones column" (fused bias gradient)
+inline int64_t n_pad(int64_t N) { return round_up(N + 1, 8); }
 inline int64_t row_elems(int64_t M, int64_t N) { return m_pad(M) + n_pad(N); }
 inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4; }
 
@@ -81,9 +82,10 @@ cudaError_t launch_sfb_simt(int64_t M, int64_t N, int64_t KP, int32_t dtype, con
                             cudaStream_t s);
 // tcgen05 / TMEM / TMA reconstruct-and-apply (POS_DT_BF16 / POS_DT_TF32). Returns
 // cudaErrorNotSupported if the shape/alignment cannot use TMA (caller falls back to SIMT).
+// b != nullptr: the bias update is fused (needs the ones column of the packed v rows).
 cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
-                          int32_t accumulate, float* W, int64_t ldw, float alpha, int max_ctas,
-                          cudaStream_t s);
+                          int32_t accumulate, float* W, int64_t ldw, float* b, float alpha,
+                          int max_ctas, cudaStream_t s);
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G);
 
 // A launch plan for the tensor-core reconstruct-and-apply: TMA descriptors encoded once for fixed
@@ -96,10 +98,11 @@ struct SfbTcPlan {
   // device scratch (2 x u32, zero-initialised, owned by the plan's creator) for the dynamic tile
   // scheduler; nullptr = static round-robin tiles. Launches sharing a counter must not overlap.
   unsigned int* counter = nullptr;
+  float* bias = nullptr;   // fused A4b target (nullptr = no bias)
 };
 // false if the shape/alignment/dtype cannot use the tensor-core kernel
 bool sfb_tc_make_plan(SfbTcPlan* plan, int64_t M, int64_t N, int64_t KP, int32_t dtype,
-                      const void* G, float* W, int64_t ldw, int max_ctas);
+                      const void* G, float* W, int64_t ldw, int max_ctas, float* bias = nullptr);
 cudaError_t sfb_tc_launch(const SfbTcPlan& plan, float alpha, int accumulate, cudaStream_t s);
 
 // A4 + A4b dispatcher used by the C ABI and the context code

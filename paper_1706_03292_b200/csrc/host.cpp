@@ -194,14 +194,15 @@ int reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const voi
   POS_CHECK_ARG(aligned16(G), "G must be 16-byte aligned");
   POS_CHECK_ARG((M * ldw) / ldw == M, "M * ldw overflows");
   cudaError_t e;
-  if (dtype != POS_DT_F32 && sfb_tc_supported(N, ldw, W, G)) {
-    e = launch_sfb_tc(M, N, KP, dtype, G, accumulate, W, ldw, alpha, max_ctas, s);
+  const bool tc = dtype != POS_DT_F32 && sfb_tc_supported(N, ldw, W, G);
+  if (tc) {   // bias fused into the tensor-core epilogue (ones column)
+    e = launch_sfb_tc(M, N, KP, dtype, G, accumulate, W, ldw, b, alpha, max_ctas, s);
   } else {
     e = launch_sfb_simt(M, N, KP, dtype, G, accumulate, W, ldw, alpha, s);
   }
   if (e != cudaSuccess)
     POS_FAIL(POS_ECUDA, "reconstruct kernel launch failed: %s", cudaGetErrorString(e));
-  if (b) {
+  if (b && !tc) {
     e = launch_bias_colsum(M, N, KP, dtype, G, accumulate, b, alpha, s);
     if (e != cudaSuccess)
       POS_FAIL(POS_ECUDA, "bias kernel launch failed: %s", cudaGetErrorString(e));

@@ -32,11 +32,14 @@ __global__ void pack_bf16_kernel(const Tin* __restrict__ u, const Tin* __restric
   int64_t idx, lim;
   if (col < Mp) { src = u + k * M; idx = col; lim = M; }
   else          { src = v + k * N; idx = col - Mp; lim = N; }
+  // v's first pad column (index N) holds 1.0: the reconstruction's extra output column is then
+  // sum_j u_j, the bias gradient (A4b fused into A4); every other pad element is 0
+  const int64_t onec = col < Mp ? -1 : N;
   __align__(16) __nv_bfloat16 o[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t j = idx + i;
-    o[i] = __float2bfloat16_rn(j < lim ? ld_in(src + j) : 0.0f);
+    o[i] = __float2bfloat16_rn(j < lim ? ld_in(src + j) : (j == onec ? 1.0f : 0.0f));
   }
   *reinterpret_cast<uint4*>(out + k * R + col) = *reinterpret_cast<const uint4*>(o);
 }
@@ -53,11 +56,14 @@ __global__ void pack_f32_kernel(const Tin* __restrict__ u, const Tin* __restrict
   int64_t idx, lim;
   if (col < Mp) { src = u + k * M; idx = col; lim = M; }
   else          { src = v + k * N; idx = col - Mp; lim = N; }
+  // v's first pad column (index N) holds 1.0: the reconstruction's extra output column is then
+  // sum_j u_j, the bias gradient (A4b fused into A4); every other pad element is 0
+  const int64_t onec = col < Mp ? -1 : N;
   float4 o;
-  o.x = idx + 0 < lim ? ld_in(src + idx + 0) : 0.0f;
-  o.y = idx + 1 < lim ? ld_in(src + idx + 1) : 0.0f;
-  o.z = idx + 2 < lim ? ld_in(src + idx + 2) : 0.0f;
-  o.w = idx + 3 < lim ? ld_in(src + idx + 3) : 0.0f;
+  o.x = idx + 0 < lim ? ld_in(src + idx + 0) : (idx + 0 == onec ? 1.0f : 0.0f);
+  o.y = idx + 1 < lim ? ld_in(src + idx + 1) : (idx + 1 == onec ? 1.0f : 0.0f);
+  o.z = idx + 2 < lim ? ld_in(src + idx + 2) : (idx + 2 == onec ? 1.0f : 0.0f);
+  o.w = idx + 3 < lim ? ld_in(src + idx + 3) : (idx + 3 == onec ? 1.0f : 0.0f);
   *reinterpret_cast<float4*>(out + k * R + col) = o;
 }
 

@@ -205,14 +205,12 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
     if (ts && (rc = trec(ts->a0, as))) return rc;
     if (un.plan_ctas != c->max_ctas) {   // (re)build the cached launch plan
       un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * P, un.dtype, un.gbuf, un.W,
-                                     un.N, c->max_ctas);
+                                     un.N, c->max_ctas, un.b);
       un.plan.counter = (s->flags & POS_SCHED_STATIC_TILES) ? nullptr : un.tile_counter;
       un.plan_ctas = c->max_ctas;
     }
     if (un.has_plan) {
-      cudaError_t e2 = sfb_tc_launch(un.plan, s->alpha, 1, as);
-      if (e2 == cudaSuccess && un.b)
-        e2 = launch_bias_colsum(un.M, un.N, un.K * P, un.dtype, un.gbuf, 1, un.b, s->alpha, as);
+      cudaError_t e2 = sfb_tc_launch(un.plan, s->alpha, 1, as);   // bias fused
       if (e2 != cudaSuccess) return ctx_cuda_fail(c, e2, "reconstruct launch");
     } else {
       rc = reconstruct_apply(un.M, un.N, un.K * P, un.dtype, un.gbuf, 1, un.W, un.N, un.b,

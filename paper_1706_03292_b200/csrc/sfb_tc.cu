@@ -201,6 +201,7 @@ struct TileInfo {
   // Self-resetting: the last CTA to finish zeroes both, so the counter is reusable by the next
   // launch on the same stream (and by every CUDA-graph replay).
   unsigned int* counter;
+  float* bias;     // fused A4b: b (+)= alpha * accumulator column N; nullptr = no bias
 };
 
 template <bool kTF32>
@@ -383,6 +384,24 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const int nsub = nsub_of(ti.N, n0);
       mbar_wait(b_tfull + 8 * acc, aphase);
       tc_fence_after();
+      // A4b fused: the gathered v rows carry a 1.0 in column N, so accumulator column N of the
+      // tile holding it is sum_j U[j][m] — the bias gradient of row m
+      if (ti.bias && (int64_t)n0 <= ti.N && ti.N < (int64_t)n0 + BN) {
+        uint32_t bv;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                     : "=r"(bv)
+                     : "r"(tmem_base + lane_addr + acc * BN + (uint32_t)(ti.N - n0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int64_t m = (int64_t)m0 + et;
+        if (m < ti.M) {
+          const float base = accumulate ? ti.bias[m] : 0.0f;
+          ti.bias[m] = fmaf(alpha, __uint_as_float(bv), base);
+        }
+      }
+      if (nsub == 0) {                        // bias-only tile: nothing else reads TMEM
+        tc_fence_before();
+        mbar_arrive(b_tempty + 8 * acc);
+      }
       for (int j = 0; j < nsub; ++j) {
         uint32_t r[32];
         tmem_ld32(tmem_base + lane_addr + acc * BN + j * WSUB, r);
@@ -470,7 +489,9 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 
 template <bool kTF32>
 bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
-                    int64_t ldw, int max_ctas) {
+                    int64_t ldw, int max_ctas, float* bias) {
+  // with a bias the V operand includes the ones column N (the GEMM's extra output column)
+  const int64_t NB = N + (bias ? 1 : 0);
   constexpr int EB = kTF32 ? 4 : 2;
   constexpr int BK = KBYTES / EB, CHUNK = SWZ / EB;
   const int64_t R = row_elems(M, N), Mp = m_pad(M);
@@ -482,13 +503,14 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
   const uint8_t* g = static_cast<const uint8_t*>(G);
   if (!encode_2d(&pl->tmA, dt, g, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK,
                  oswz) ||
-      !encode_2d(&pl->tmB, dt, g + Mp * EB, (uint64_t)N, (uint64_t)KP, (uint64_t)(R * EB),
+      !encode_2d(&pl->tmB, dt, g + Mp * EB, (uint64_t)NB, (uint64_t)KP, (uint64_t)(R * EB),
                  CHUNK, BK, oswz) ||
       !encode_2d(&pl->tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, W, (uint64_t)N, (uint64_t)M,
                  (uint64_t)(ldw * 4), WSUB, BM))
     return false;
   pl->M = M; pl->N = N; pl->KP = KP;
-  pl->nb_n = (int)((N + BN - 1) / BN);
+  pl->nb_n = (int)((NB + BN - 1) / BN);
+  pl->bias = bias;
   const int64_t tiles = (int64_t)pl->nb_n * ((M + BM - 1) / BM);
   if (tiles > INT32_MAX) return false;
   pl->num_tiles = (int)tiles;
@@ -515,6 +537,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   ti.M = pl.M; ti.N = pl.N; ti.KP = pl.KP;
   ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
   ti.counter = pl.counter;
+  ti.bias = pl.bias;
   sfb_tc_kernel<kTF32><<<pl.grid, THREADS, SMEM_TOTAL, s>>>(pl.tmA, pl.tmB, pl.tmW, ti, alpha,
                                                               accumulate);
   return cudaGetLastError();
@@ -530,10 +553,10 @@ bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
 }
 
 bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t dtype,
-                      const void* G, float* W, int64_t ldw, int max_ctas) {
+                      const void* G, float* W, int64_t ldw, int max_ctas, float* bias) {
   if (dtype == POS_DT_F32 || !sfb_tc_supported(N, ldw, W, G)) return false;
-  if (dtype == POS_DT_TF32) return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas);
-  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas);
+  if (dtype == POS_DT_TF32) return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas, bias);
+  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas, bias);
 }
 
 cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
@@ -542,10 +565,10 @@ cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cuda
 }
 
 cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
-                          int32_t accumulate, float* W, int64_t ldw, float alpha, int max_ctas,
-                          cudaStream_t s) {
+                          int32_t accumulate, float* W, int64_t ldw, float* b, float alpha,
+                          int max_ctas, cudaStream_t s) {
   SfbTcPlan pl;
-  if (!sfb_tc_make_plan(&pl, M, N, KP, dtype, G, W, ldw, max_ctas)) return cudaErrorInvalidValue;
+  if (!sfb_tc_make_plan(&pl, M, N, KP, dtype, G, W, ldw, max_ctas, b)) return cudaErrorInvalidValue;
   return sfb_tc_launch(pl, alpha, accumulate, s);
 }
 

@@ -138,17 +138,19 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, const Tin* __r
     int64_t idx, lim;
     if (col < Mp) { src = u + k * M; idx = col; lim = M; }
     else          { src = v + k * N; idx = col - Mp; lim = N; }
+    const int64_t onec = col < Mp ? -1 : N;   // ones column (fused bias), as in pack_*_kernel
     float4 o;
     if constexpr (kBF16) {
       __align__(16) __nv_bfloat16 h[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) h[i] = __float2bfloat16_rn(idx + i < lim ? ld_in(src + idx + i) : 0.f);
+      for (int i = 0; i < 8; ++i)
+        h[i] = __float2bfloat16_rn(idx + i < lim ? ld_in(src + idx + i) : (idx + i == onec ? 1.f : 0.f));
       o = *reinterpret_cast<const float4*>(h);   // bit pattern only; a store does not convert
     } else {
-      o.x = idx + 0 < lim ? ld_in(src + idx + 0) : 0.f;
-      o.y = idx + 1 < lim ? ld_in(src + idx + 1) : 0.f;
-      o.z = idx + 2 < lim ? ld_in(src + idx + 2) : 0.f;
-      o.w = idx + 3 < lim ? ld_in(src + idx + 3) : 0.f;
+      o.x = idx + 0 < lim ? ld_in(src + idx + 0) : (idx + 0 == onec ? 1.f : 0.f);
+      o.y = idx + 1 < lim ? ld_in(src + idx + 1) : (idx + 1 == onec ? 1.f : 0.f);
+      o.z = idx + 2 < lim ? ld_in(src + idx + 2) : (idx + 2 == onec ? 1.f : 0.f);
+      o.w = idx + 3 < lim ? ld_in(src + idx + 3) : (idx + 3 == onec ? 1.f : 0.f);
     }
     // element offset of this 16-byte vector in float units: (k * R + col) * eb / 4
     mm_st_v4(dst + ((k * R + col) * (kBF16 ? 2 : 4)) / 4, o);

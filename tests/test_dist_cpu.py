@@ -88,6 +88,7 @@ def _sfb_worker(rank, world):
     slot = np.zeros((K, R), np.float32)
     slot[:, :M] = u
     slot[:, Mp:Mp + N] = v
+    slot[:, Mp + N] = 1.0          # the ones column of the ABI layout (bias gradient column)
     gathered = [torch.zeros(K, R) for _ in range(world)]
     dist.all_gather(gathered, torch.from_numpy(slot))
     G = np.concatenate([g.numpy() for g in gathered])          # rows j = p*K + k
@@ -96,7 +97,10 @@ def _sfb_worker(rank, world):
     W0 = si.exact_weights(si.rng(51, 1), M, N)
     ref, _ = sync.sfb_update(W0, None, Us, Vs, si.EXACT_ALPHA)
     assert np.array_equal(W0 + si.EXACT_ALPHA * (U.T @ V), ref)
-    assert not np.any(G[:, M:Mp]) and not np.any(G[:, Mp + N:])   # pads stay zero
+    # the ones column turns the same contraction into the bias gradient: (U^T 1)[m] = sum_j u_j[m]
+    ones = G[:, Mp + N].astype(np.float64)
+    assert np.array_equal(U.T @ ones, np.sum(np.concatenate(Us).astype(np.float64), axis=0))
+    assert not np.any(G[:, M:Mp]) and not np.any(G[:, Mp + N + 1:])   # other pads stay zero
 
 
 def _uid_worker(rank, world):

@@ -269,4 +269,5 @@ def test_pack_layout(dtype):
     exp = torch.zeros(K, R, dtype=tdt)
     exp[:, :M] = torch.from_numpy(u).to(tdt)          # torch's CPU RNE cast
     exp[:, 16:16 + N] = torch.from_numpy(v).to(tdt)
+    exp[:, 16 + N] = 1.0                              # ones column (fused bias gradient)
     assert torch.equal(slot.cpu(), exp)
