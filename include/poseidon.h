@@ -101,7 +101,7 @@ int pos_shard_range(int64_t n, int32_t P, int32_t r, int64_t* begin, int64_t* en
 /* Elements a caller must allocate for a PS layer's W and grad buffers: P * S. */
 int64_t pos_padded_size(int64_t n, int32_t P);
 /* Row length (elements) of the library's gathered factor layout for an FC layer:
- * M_pad + N_pad with M_pad = ceil(M/8)*8, N_pad = ceil((N+1)/8)*8 (16-byte TMA row rule; column N
+ * M_pad + N_pad with M_pad = ceil(M/64)*64, N_pad = ceil((N+1)/64)*64 (128-byte aligned rows; column N
  * of the v part is the "ones column" that makes the reconstruction GEMM also produce the bias
  * gradient sum_j u_j, reading S12). */
 int64_t pos_factor_row_elems(int64_t M, int64_t N);

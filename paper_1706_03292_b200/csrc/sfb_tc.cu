@@ -7,16 +7,19 @@
 // gathered factor rows stacked as U (KP x M) and V (KP x N) that is the dense contraction
 // U^T V with inner dimension KP, fused here with the SGD apply of PAPER:107 ("apply (+)").
 //
-// Design (DESIGN.md §A4):
-//  * persistent, warp-specialised CTA, one per SM; 128 x 256 output tile; tiles in static
-//    round-robin order (deterministic, no split-K, no atomics -> bitwise-identical replicas);
+// Design (DESIGN.md §5):
+//  * persistent, warp-specialised CTA, one per SM; 128 x 256 output tile; tiles handed out by a
+//    dynamic atomic tile scheduler (or static round-robin); no split-K, no atomics on data: a
+//    tile's arithmetic never depends on which CTA computes it -> bitwise-identical replicas;
 //  * operands U, V streamed by TMA (128-byte swizzle, MN-major: m / n is the contiguous
-//    direction of the gathered rows) into a 3-stage smem ring, consumed by tcgen05.mma issued by
-//    one thread, accumulating in TMEM (fp32). Two 256-column TMEM accumulators: the epilogue of
-//    tile i overlaps the MMAs of tile i+1;
+//    direction of the gathered rows; 128-byte aligned rows) into a 3-stage smem ring, consumed
+//    by tcgen05.mma issued by one thread, accumulating in TMEM (fp32). Two 256-column TMEM
+//    accumulators: the epilogue of tile i overlaps the MMAs of tile i+1;
 //  * the W tile (the HBM-dominant traffic: 8 bytes per element) is streamed in 128 x 32 fp32
-//    sub-tiles by a second TMA producer warp into a 4-slot ring, updated in shared memory by the
-//    4 epilogue warps (tcgen05.ld 32x32b -> fma -> st.shared) and written back by TMA store.
+//    sub-tiles by a second TMA producer warp into a 5-slot ring, updated in shared memory by the
+//    4 epilogue warps (tcgen05.ld 32x32b -> fma -> st.shared) and written back by TMA store;
+//  * the bias gradient comes out of the same GEMM: the packed v rows carry a 1.0 in column N,
+//    so accumulator column N is sum_j u_j (A4b fused; read with one tcgen05.ld 32x32b.x1).
 //
 // Warp roles (256 threads): w0 operand TMA producer, w1 MMA issuer + TMEM owner, w2 W TMA
 // producer, w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes 32*(w%4) .. +31 = tile rows).
@@ -101,6 +104,32 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
                ::"l"(map), "r"(c0), "r"(c1), "r"(src)
                : "memory");
+}
+// L2 cache-policy variants: W is streamed exactly once (evict first, so it does not displace the
+// operands U, V that every CTA re-reads; its dirty lines also leave L2 sooner).
+#ifndef POS_SFB_L2HINT
+#define POS_SFB_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint32_t bar,
+                                                 uint32_t dst, int32_t c0, int32_t c1,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, uint32_t src,
+                                                  int32_t c0, int32_t c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint"
+      " [%0, {%1, %2}], [%3], %4;" ::"l"(map), "r"(c0), "r"(c1), "r"(src), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;"); }
 template <int N>
@@ -358,7 +387,10 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const uint32_t wf = b_wfull + 8 * ws;
           if (accumulate) {
             mbar_expect_tx(wf, W_BYTES);
-            tma_load_2d(&tmW, wf, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
+            if (POS_SFB_L2HINT)
+              tma_load_2d_hint(&tmW, wf, sW0 + ws * W_BYTES, n0 + j * WSUB, m0, policy_evict_first());
+            else
+              tma_load_2d(&tmW, wf, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
           } else {
             mbar_arrive(wf);
           }
@@ -432,7 +464,10 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         fence_proxy_async_smem();             // generic-proxy smem writes -> visible to TMA
         named_bar_sync(1, 128);
         if (et == 0) {
-          tma_store_2d(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
+          if (POS_SFB_L2HINT)
+            tma_store_2d_hint(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0, policy_evict_first());
+          else
+            tma_store_2d(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
           bulk_commit();
           if (pending >= 0) {
             bulk_wait_read<1>();              // the previous store has finished reading smem

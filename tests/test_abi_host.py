@@ -112,8 +112,8 @@ def test_shard_table_bit_exact():
 
 
 def test_factor_row_layout():
-    # M_pad = ceil(M/8)*8; N_pad = ceil((N+1)/8)*8 (room for the ones column)
-    assert pos.pos_factor_row_elems(21841, 4096) == 21848 + 4104
-    assert pos.pos_factor_row_elems(1, 1) == 16
-    assert pos.pos_factor_row_elems(64, 64) == 64 + 72
-    assert pos.pos_factor_row_elems(13, 7) == 16 + 8
+    # M_pad = ceil(M/64)*64; N_pad = ceil((N+1)/64)*64 (128-byte rows, room for the ones column)
+    assert pos.pos_factor_row_elems(21841, 4096) == 21888 + 4160
+    assert pos.pos_factor_row_elems(1, 1) == 64 + 64
+    assert pos.pos_factor_row_elems(64, 64) == 64 + 128
+    assert pos.pos_factor_row_elems(13, 7) == 64 + 64

@@ -83,7 +83,7 @@ def _sfb_worker(rank, world):
     from oracle import sync
     K, M, N = 4, 13, 7
     R = pos.pos_factor_row_elems(M, N)
-    Mp = (M + 7) // 8 * 8
+    Mp = (M + 63) // 64 * 64
     u, v = si.exact_factors(si.rng(51, 0, rank), K, M, N)
     slot = np.zeros((K, R), np.float32)
     slot[:, :M] = u

@@ -86,7 +86,7 @@ def test_pack_writes_only_its_slot(M, N, K):
     torch.cuda.synchronize()
     assert bool(torch.all(out[:G] == 3.0)) and bool(torch.all(out[G + K * R:] == 3.0))
     slot = out[G:G + K * R].view(K, R).float().cpu().numpy()
-    Mp = (M + 7) // 8 * 8
+    Mp = (M + 63) // 64 * 64
     assert np.array_equal(slot[:, :M], u) and np.array_equal(slot[:, Mp:Mp + N], v)
     assert not slot[:, M:Mp].any() and not slot[:, Mp + N + 1:].any()
     assert np.all(slot[:, Mp + N] == 1.0)          # ones column (fused bias)

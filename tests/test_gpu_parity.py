@@ -260,7 +260,7 @@ def test_pack_layout(dtype):
     u = g.standard_normal((K, M)).astype(np.float32)
     v = g.standard_normal((K, N)).astype(np.float32)
     R = pos.pos_factor_row_elems(M, N)
-    assert R == 16 + 8
+    assert R == 64 + 64
     ud, vd = to_dev(u), to_dev(v)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     slot = torch.full((K, R), 99.0, dtype=tdt, device="cuda")
@@ -268,6 +268,6 @@ def test_pack_layout(dtype):
     torch.cuda.synchronize()
     exp = torch.zeros(K, R, dtype=tdt)
     exp[:, :M] = torch.from_numpy(u).to(tdt)          # torch's CPU RNE cast
-    exp[:, 16:16 + N] = torch.from_numpy(v).to(tdt)
-    exp[:, 16 + N] = 1.0                              # ones column (fused bias gradient)
+    exp[:, 64:64 + N] = torch.from_numpy(v).to(tdt)
+    exp[:, 64 + N] = 1.0                              # ones column (fused bias gradient)
     assert torch.equal(slot.cpu(), exp)
