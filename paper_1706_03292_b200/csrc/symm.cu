@@ -70,7 +70,10 @@ __device__ __forceinline__ void mm_st(float* p, float v) {
 }
 
 constexpr int kPsThreads = 512;
-constexpr int kPsUnroll = 4;
+#ifndef POS_NVLS_UNROLL
+#define POS_NVLS_UNROLL 4
+#endif
+constexpr int kPsUnroll = POS_NVLS_UNROLL;   // 16-byte NVLS reductions in flight per thread
 
 __global__ void __launch_bounds__(kPsThreads)
 ps_nvls_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, size_t off_w,

@@ -6,7 +6,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1706_03292_b200 as pos
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
-shapes = [(4096, 25088, 32), (21841, 4096, 32), (4096, 4096, 32), (4096, 25088, 256), (21841, 4096, 256), (4096, 9216, 1024)]
+shapes = [(4096, 25088, 32), (21841, 4096, 32), (4096, 4096, 32), (4096, 25088, 256), (21841, 4096, 256), (4096, 9216, 512), (4096, 9216, 1024)]
+if os.environ.get("A4_SHAPES"):
+    shapes = [tuple(map(int, x.split(","))) for x in os.environ["A4_SHAPES"].split(";")]
 tag = os.environ.get("TAG", os.path.basename(pos.LIB_PATH))
 for (M, N, KP) in shapes:
     R = pos.pos_factor_row_elems(M, N)

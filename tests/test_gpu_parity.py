@@ -147,6 +147,36 @@ def test_tile_edges_exact_bitwise_k_p(MN, K, P, dtype):
     assert np.array_equal(bg, br)
 
 
+# ------------------------------------------------------- CTA-pair kernel (cta_group::2) ----
+# The pair kernel (256-row tiles, each CTA holding half of the V columns) is chosen for
+# K*P >= 256; POS_SFB_PAIR=1 / 0 forces it on / off at plan time so that both kernels are
+# checked on the same ragged shapes.
+PAIR_MN = [(1, 4), (65, 129), (129, 260), (255, 132), (257, 1028), (1000, 4100), (4097, 64)]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("KP", [(1, 1), (8, 2), (32, 8), (40, 7)])
+@pytest.mark.parametrize("MN", PAIR_MN)
+def test_pair_kernel_exact_bitwise(MN, KP, dtype, monkeypatch):
+    monkeypatch.setenv("POS_SFB_PAIR", "1")
+    (M, N), (K, P) = MN, KP
+    _, _, Wg, bg, Wr, br = run_sfb(P, K, M, N, dtype, "f32", "exact", seed=M + N + K)
+    assert np.array_equal(Wg, Wr), (M, N, K, P)
+    assert np.array_equal(bg, br)
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_pair_and_single_kernels_statistical_large_kp(pair, dtype, monkeypatch):
+    """K*P = 512 (AlexNet-like fc7 at P = 4): both kernels within the north_star tolerance."""
+    monkeypatch.setenv("POS_SFB_PAIR", pair)
+    W, _, Wg, bg, Wr, br = run_sfb(4, 128, 1000, 1028, dtype, "bf16" if dtype == "bf16" else "f32",
+                                   "stat", seed=5)
+    assert err(Wg, Wr) <= TOL[dtype]
+    assert err(Wg - W, Wr - W) <= TOL[dtype]
+    assert err(bg, br) <= TOL[dtype]
+
+
 # ---------------------------------------------------------------------- full-size layers ----
 @pytest.mark.parametrize("layer", [(4096, 25088, 32, 1), (21841, 4096, 32, 1), (4096, 4096, 32, 8),
                                    (1000, 4096, 32, 2)])

@@ -294,10 +294,13 @@ def test_sched_dense_bucket(timing):
     ctx.close()
 
 
-def test_sched_dynamic_tiles_bitwise_equal_static_and_repeatable():
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_sched_dynamic_tiles_bitwise_equal_static_and_repeatable(pair, monkeypatch):
     """The dynamic tile scheduler (atomic tile fetch, self-resetting counter) changes which CTA
     computes a tile, never the tile's arithmetic: bitwise equal to the static order, over repeated
-    iterations (the counter must reset after every launch)."""
+    iterations (the counter must reset after every launch). pair = "1": the CTA-pair kernel, whose
+    leader CTA fetches tiles and broadcasts them to its peer through distributed shared memory."""
+    monkeypatch.setenv("POS_SFB_PAIR", pair)
     model = make_model(5)
     a = si.EXACT_ALPHA
     dyn, _, _ = run(model, a)
