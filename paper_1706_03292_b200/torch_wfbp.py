@@ -10,7 +10,7 @@ APIs in between gradient generation and application (L7)". Here:
   applies it (A4).
 * every other parameterised module (Conv2d, BatchNorm) is a DENSE layer: its parameters become
   views into flat bucket buffers (library-symmetric when P > 1), .grad views into matching gradient
-  buckets; a post-accumulate-grad hook fires pos_sched_grad_ready once all of the module's
+  buckets; a post-accumulate-grad hook fires pos_sched_grad_ready once all of the bucket's
   parameters have their gradient.
 * Wfbp.step(loss) = Algorithm 2: begin (C := 0), loss.backward() (triggers in L..1 order as autograd
   reaches each layer), end (the current stream waits until every layer is applied).
@@ -97,45 +97,56 @@ class Wfbp:
                 continue
             layers.append(mod)
         self.layers = layers
-        self.sched = Scheduler(ctx, len(layers), timing=timing, sequential=sequential)
-        self._keep = []              # factors alive until the iteration ends
-        self._buffers = []
+        # Scheduler layers: one per FC layer, one per bucket of consecutive dense modules (a bucket
+        # is triggered once, by the last of its parameters' post-accumulate-grad hooks, so the host
+        # pays one library call per bucket, not per module).
+        units = []
         bucket_elems = int(bucket_mb * 2 ** 20 / 4)
-        in_dt = POS_IN_BF16 if factor_dtype == torch.bfloat16 else POS_IN_F32
         i = 0
         while i < len(layers):
-            mod = layers[i]
-            if isinstance(mod, PosLinear):
-                M, N = mod.out_features, mod.in_features
-                scheme = self.sched.add_fc(i, M, N, self.K, mod.weight.data, None if mod.bias is None else mod.bias.data,
-                                           None, dtype=dtype, in_dtype=in_dt)
-                if scheme != POS_SCHEME_SFB:
-                    raise NotImplementedError("FC layer on the PS path needs a flat [W|b] buffer")
-                mod._wfbp, mod._wfbp_index = self, i
-                mod.weight.requires_grad_(False)   # dW is never formed by autograd
-                if mod.bias is not None:
-                    mod.bias.requires_grad_(False)
-                # the forward must still see the layer as trainable for grad_input: x requires grad
+            if isinstance(layers[i], PosLinear):
+                units.append(("fc", layers[i]))
                 i += 1
                 continue
-            # a bucket of consecutive dense modules
             group, n_tot = [], 0
             while i < len(layers) and not isinstance(layers[i], PosLinear):
                 m = layers[i]
                 n_m = sum(p.numel() for p in m.parameters(recurse=False) if p.requires_grad)
-                group.append((i, m, n_m))
+                group.append(m)
                 n_tot += n_m
                 i += 1
                 if n_tot >= bucket_elems:
                     break
+            units.append(("dense", group, n_tot))
+        self.sched = Scheduler(ctx, len(units), timing=timing, sequential=sequential)
+        self._keep = []              # factors alive until the iteration ends
+        self._buffers = []
+        self._pending = [0] * len(units)   # parameters of each bucket still without a gradient
+        self._nparams = [0] * len(units)
+        in_dt = POS_IN_BF16 if factor_dtype == torch.bfloat16 else POS_IN_F32
+        for ui, un in enumerate(units):
+            if un[0] == "fc":
+                mod = un[1]
+                M, N = mod.out_features, mod.in_features
+                scheme = self.sched.add_fc(ui, M, N, self.K, mod.weight.data, None if mod.bias is None else mod.bias.data,
+                                           None, dtype=dtype, in_dtype=in_dt)
+                if scheme != POS_SCHEME_SFB:
+                    raise NotImplementedError("FC layer on the PS path needs a flat [W|b] buffer")
+                mod._wfbp, mod._wfbp_index = self, ui
+                mod.weight.requires_grad_(False)   # dW is never formed by autograd
+                if mod.bias is not None:
+                    mod.bias.requires_grad_(False)
+                # the forward must still see the layer as trainable for grad_input: x requires grad
+                continue
+            _, group, n_tot = un
             Pn = pos_padded_size(n_tot, self.P)
             if self.P > 1:
                 Wf, Gf = ctx.sym_empty(Pn), ctx.sym_empty(Pn)
             else:
                 Wf, Gf = torch.zeros(Pn, device=dev), torch.zeros(Pn, device=dev)
             off = 0
-            for (li, m, n_m) in group:
-                m._wfbp_pending = 0
+            hook = self._make_hook(ui)
+            for m in group:
                 for p in m.parameters(recurse=False):
                     if not p.requires_grad:
                         continue
@@ -146,18 +157,19 @@ class Wfbp:
                     wv.copy_(p.data)
                     p.data = wv
                     p.grad = torch.as_strided(Gf, p.shape, p.stride(), off)
-                    p.register_post_accumulate_grad_hook(self._make_hook(li, m))
-                    m._wfbp_pending += 1
+                    p.register_post_accumulate_grad_hook(hook)
+                    self._nparams[ui] += 1
                     off += k
-                m._wfbp_nparams = m._wfbp_pending
-            self.sched.add_dense_bucket(group[0][0], [g[2] for g in group], Wf, Gf)
+            self.sched.add_dense_bucket(ui, [n_tot], Wf, Gf)
             self._buffers.append((Wf, Gf))
 
-    def _make_hook(self, li, mod):
+    def _make_hook(self, ui):
+        pending, sched = self._pending, self.sched
+
         def hook(p):
-            mod._wfbp_pending -= 1
-            if mod._wfbp_pending == 0:
-                self.sched.grad_ready(li, torch.cuda.current_stream())
+            pending[ui] -= 1
+            if pending[ui] == 0:
+                sched.grad_ready(ui, torch.cuda.current_stream())
         return hook
 
     def factors_ready(self, li, u, v):
@@ -172,9 +184,7 @@ class Wfbp:
 
     def step(self, loss, lr: float):
         """One Algorithm-2 iteration: C := 0, backward (per-layer triggers), wait until all applied."""
-        for m in self.layers:
-            if hasattr(m, "_wfbp_nparams"):
-                m._wfbp_pending = m._wfbp_nparams
+        self._pending[:] = self._nparams
         self.zero_grad()
         self.sched.begin(-lr / self.P)
         loss.backward()

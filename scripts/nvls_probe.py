@@ -27,10 +27,11 @@ for mb in [4, 19, 80]:
     y = torch.empty(Pn // world, device=dev)
     t_rs = timeit(lambda: dist.reduce_scatter_tensor(y, Gd))
     t_ag = timeit(lambda: dist.all_gather_into_tensor(Gd, y))
+    t_ar = timeit(lambda: dist.all_reduce(Gd))
     # per-rank NVLink bytes per direction of the PS exchange (ring RS + AG): 2 (P-1)/P n 4
     nvl = 2 * (world - 1) / world * n * 4
     if rank == 0:
         print(json.dumps({"tag": tag, "P": world, "MB": mb, "nvls_us": round(t_nvls, 1), "nccl_ps_us": round(t_nccl, 1),
-                          "torch_rs_us": round(t_rs, 1), "torch_ag_us": round(t_ag, 1),
+                          "torch_rs_us": round(t_rs, 1), "torch_ag_us": round(t_ag, 1), "torch_allreduce_us": round(t_ar, 1),
                           "nvls_GBs_ringequiv": round(nvl / t_nvls / 1e3), "nccl_GBs": round(nvl / t_nccl / 1e3)}), flush=True)
 ctx.close(); dist.destroy_process_group()

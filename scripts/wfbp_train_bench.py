@@ -1,8 +1,12 @@
 """Exposed synchronisation time of a real training step (SURVEY §8(d) "Exposed sync"; the north
 star's third target): VGG19-22K (or another config) forward + backward at batch K per GPU, bf16
 autocast, channels_last, synthetic images and labels, with Poseidon's per-layer synchronisation
-driven by autograd hooks (WFBP), versus the same compute with the synchronisation off, and versus
-the sequential schedule (sync after the whole backward, the Caffe+PS analogue of PAPER:407).
+driven by autograd hooks (WFBP), versus
+  local:   the plain single-GPU PyTorch step doing the same update (autograd dW + SGD, no sync) —
+           the baseline the exposed fraction is quoted against ("exposed_frac_wfbp_vs_local");
+  nosync:  the same forward/backward without dW or any update (a lower bound, not a real step);
+and versus the sequential schedule (sync after the whole backward, the Caffe+PS analogue of
+PAPER:407).
 
     python scripts/wfbp_train_bench.py [--config c3] [--steps 20]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 scripts/wfbp_train_bench.py
@@ -51,6 +55,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--bucket-mb", type=float, default=16.0)
     ap.add_argument("--max-ctas", type=int, default=-1, help="cap of the reconstruction grid (0 = all SMs)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the whole training step (forward, backward, synchronisation) as one CUDA "
+                         "graph: no host launch overhead in either arm, so the difference is the sync itself")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -71,8 +78,12 @@ def main():
 
     def run(mode):
         model, res, ncls = build_model(model_name, dev)
-        wf = None
-        if mode == "nosync":
+        wf = opt = None
+        if mode == "local":
+            # plain single-GPU PyTorch training step with the same update: autograd dW for every
+            # layer + SGD (foreach) — the work a step does without any synchronisation
+            opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.0, foreach=True)
+        elif mode == "nosync":
             convert_linear(model)
             for mod in model.modules():                 # same compute: no dW for FC layers
                 if isinstance(mod, nn.Linear):
@@ -89,7 +100,11 @@ def main():
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 out = model(x)
                 loss = lossf(out.float(), y)
-            if wf is None:
+            if opt is not None:
+                opt.zero_grad(set_to_none=True)
+                loss.backward()
+                opt.step()
+            elif wf is None:
                 for p in model.parameters():
                     p.grad = None
                 loss.backward()
@@ -100,12 +115,32 @@ def main():
         for _ in range(a.warmup):
             step()
         torch.cuda.synchronize()
+        run_step = step
+        if a.graph:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _ in range(3):
+                    step()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                g_loss = step()
+            torch.cuda.synchronize()
+
+            def run_step():
+                gph.replay()
+                return g_loss
+            for _ in range(3):
+                run_step()
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier(device_ids=[local])
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
         for _ in range(a.steps):
-            loss = step()
+            loss = run_step()
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
@@ -114,21 +149,27 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = t.item()
         lv = float(loss.item())
+        run_step = gph = None            # the graph references the scheduler's events
+        torch.cuda.synchronize()
         if wf is not None:
             wf.close()
         del model, wf
         torch.cuda.empty_cache()
         return ms, lv
 
+    t_local, _ = run("local")
     t_nosync, _ = run("nosync")
     t_wfbp, loss_w = run("wfbp")
     t_seq, loss_s = run("sequential") if not os.environ.get("WFBP_ONLY") else (float("nan"), 0.0)
     out = {"metric": "exposed_sync_fraction", "config": a.config, "model": model_name, "per_gpu_batch": K,
-           "n_gpus": world, "ms_step_nosync": t_nosync, "ms_step_wfbp": t_wfbp, "ms_step_sequential": t_seq,
+           "n_gpus": world, "ms_step_local_sgd": t_local,
+           "exposed_ms_wfbp_vs_local": t_wfbp - t_local, "exposed_frac_wfbp_vs_local": (t_wfbp - t_local) / t_wfbp,
+           "ms_step_nosync": t_nosync, "ms_step_wfbp": t_wfbp, "ms_step_sequential": t_seq,
            "exposed_ms_wfbp": t_wfbp - t_nosync, "exposed_frac_wfbp": (t_wfbp - t_nosync) / t_wfbp,
            "exposed_ms_sequential": t_seq - t_nosync, "exposed_frac_sequential": (t_seq - t_nosync) / t_seq,
            "loss_finite": all(map(lambda v: v == v and abs(v) < 1e4, [loss_w, loss_s])),
-           "bucket_mb": a.bucket_mb, "max_ctas": a.max_ctas, "dtype": "bf16 autocast, fp32 master weights"}
+           "bucket_mb": a.bucket_mb, "max_ctas": a.max_ctas,
+           "launch": "whole step captured as one CUDA graph" if a.graph else "eager", "dtype": "bf16 autocast, fp32 master weights"}
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
