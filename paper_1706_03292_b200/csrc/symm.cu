@@ -69,6 +69,11 @@ __device__ __forceinline__ void mm_st(float* p, float v) {
   asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+#ifndef POS_ENTRY_ORDER
+#define POS_ENTRY_ORDER cuda::memory_order_acquire
+#endif
+constexpr cuda::memory_order kEntryOrder = POS_ENTRY_ORDER;
+
 constexpr int kPsThreads = 512;
 #ifndef POS_NVLS_UNROLL
 #define POS_NVLS_UNROLL 4
@@ -79,7 +84,10 @@ __global__ void __launch_bounds__(kPsThreads)
 ps_nvls_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, size_t off_w,
                int64_t lo, int64_t hi, float alpha) {
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
-  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // every worker's gradient is in place
+  // Entry: every worker's gradient is in place. The gradients were written by kernels that have
+  // completed (stream order), i.e. they are in each GPU's L2, where NVLS reads are served: the
+  // arrival needs no release fence (POS_ENTRY_ORDER selects the order for experiments).
+  bar.sync(ncclCoopCta(), kEntryOrder);
   const float* gmc = static_cast<const float*>(ncclGetLsaMultimemPointer(wg, off_g, dc));
   float* wmc = static_cast<float*>(ncclGetLsaMultimemPointer(ww, off_w, dc));
   const float* wl = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
@@ -130,7 +138,7 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, const Tin* __r
   // Entry barrier: every rank has reached this iteration's pack on its comm stream, which (by
   // pos_sched_end's contract) is after its previous reconstruction finished reading the gather
   // buffer we are about to overwrite (cross-rank WAR).
-  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  bar.sync(ncclCoopCta(), kEntryOrder);
   float* dst = static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off_slot, dc));
   constexpr int VEC = kBF16 ? 8 : 4;
   const int64_t chunks_per_row = R / VEC, total = K * chunks_per_row;
@@ -252,6 +260,11 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   clear_stale_launch_error();
   *done = false;
   if (c->world < 2 || c->local) return POS_OK;
+  static const bool mc_off = [] {   // POS_PACK_MC=0: pack locally + NCCL all-gather instead
+    const char* e = getenv("POS_PACK_MC");
+    return e && e[0] == '0';
+  }();
+  if (mc_off) return POS_OK;
   const int64_t R = row_elems(M, N), eb = dtype_bytes(dtype);
   const size_t slot_bytes = (size_t)(K * R * eb);
   ncclWindow_t wgb;
@@ -259,7 +272,13 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   if (!symm_lookup(c, gbuf, slot_bytes * c->world, &wgb, &off)) return POS_OK;
   const size_t off_slot = off + (size_t)c->rank * slot_bytes;
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
-  const int grid = grid_for(K * (R / vec), 256, kBarriers);
+  // few CTAs: every CTA pays two cross-GPU barriers, and the stores are fire-and-forget
+  static const int pack_ctas = [] {
+    const char* e = getenv("POS_PACK_CTAS");
+    const int v = (e && *e) ? atoi(e) : 128;
+    return v < 1 ? 1 : (v > kBarriers ? kBarriers : v);
+  }();
+  const int grid = grid_for(K * (R / vec), 256, pack_ctas);
   const int64_t Mp = m_pad(M);
   const ncclDevComm& dc = state(c)->dev;
   if (dtype == POS_DT_BF16) {

@@ -17,8 +17,8 @@ def timeit(fn, iters=20):
     t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev); dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.item() * 1e3
 tag = os.environ.get("TAG", "")
-for mb in [4, 19, 80]:
-    n = mb * 2**20 // 4
+for mb in [float(x) for x in os.environ.get('PROBE_MB', '4,19,80').split(',')]:
+    n = int(mb * 2**20) // 4
     Pn = pos.pos_padded_size(n, world)
     Ws, Gs = ctx.sym_empty(Pn), ctx.sym_empty(Pn)
     Wd, Gd = torch.zeros(Pn, device=dev), torch.zeros(Pn, device=dev)
