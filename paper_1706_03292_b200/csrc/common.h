@@ -94,6 +94,11 @@ bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G);
 // buffers (the scheduler keeps one per SFB layer, so the hot path does no host-side encoding).
 struct SfbTcPlan {
   CUtensorMap tmA, tmB, tmW;
+  // double-buffered gather (flag mode): maps of the second buffer, selected in the kernel by the
+  // parity of (*gsel - 1) (the gather sequence advanced by this rank's pack); gsel == nullptr:
+  // always the first buffer
+  CUtensorMap tmA2, tmB2;
+  const unsigned* gsel = nullptr;
   int64_t M = 0, N = 0, KP = 0;
   int nb_n = 0, num_tiles = 0, nkb = 0, grid = 0;
   bool tf32 = false;
@@ -105,7 +110,8 @@ struct SfbTcPlan {
 };
 // false if the shape/alignment/dtype cannot use the tensor-core kernel
 bool sfb_tc_make_plan(SfbTcPlan* plan, int64_t M, int64_t N, int64_t KP, int32_t dtype,
-                      const void* G, float* W, int64_t ldw, int max_ctas, float* bias = nullptr);
+                      const void* G, float* W, int64_t ldw, int max_ctas, float* bias = nullptr,
+                      const void* G2 = nullptr);
 cudaError_t sfb_tc_launch(const SfbTcPlan& plan, float alpha, int accumulate, cudaStream_t s);
 
 // A4 + A4b dispatcher used by the C ABI and the context code

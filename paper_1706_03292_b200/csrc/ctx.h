@@ -48,9 +48,14 @@ void symm_destroy(pos_ctx* c);
 // (and nothing enqueued) otherwise
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                   cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done);
-// pack this rank's factors and multicast them into every rank's gather buffer (+ barrier) when the
-// gather buffer is symmetric; *done = false otherwise
+// pack this rank's factors and multicast them into every rank's gather buffer when the gather
+// buffer is symmetric; *done = false otherwise. Barrier mode (gbuf2 == nullptr): entry + exit
+// barriers. Flag mode: gbuf / gbuf2 double buffer (by iteration parity) and the P ready flags, all
+// in ONE symmetric allocation; fstate = this rank's device state (2 x u32, zeroed); no waiting —
+// the consumer calls symm_wait_gathered on its stream before reading the gather buffer.
 int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
-                 const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done);
+                 const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done,
+                 void* gbuf2 = nullptr, uint32_t* flags = nullptr, unsigned* fstate = nullptr);
+int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate, cudaStream_t s);
 
 }  // namespace pos

@@ -21,6 +21,7 @@
 //    Caffe+PS comparison of PAPER:407);
 //  * iterations may be captured into CUDA graphs: nothing here synchronises with the host while
 //    a stream is capturing, and timing events become external event nodes.
+#include <cstdlib>
 #include <vector>
 
 #include "ctx.h"
@@ -47,6 +48,12 @@ struct Unit {
   float* grad = nullptr;
   void* gbuf = nullptr;        // SFB: P*K gathered factor rows; FC-on-PS: K local rows
   bool gbuf_symm = false;      // gbuf from pos_mem_alloc (NVLS multicast target)
+  // flag-mode gather (symmetric, tensor-core path): gbuf2 = second buffer, gflags = P ready
+  // flags, all in gbuf's allocation; gstate = this rank's gather sequence + pack CTA counter
+  bool flag_mode = false;
+  void* gbuf2 = nullptr;
+  uint32_t* gflags = nullptr;
+  unsigned* gstate = nullptr;
   pos::SfbTcPlan plan;         // cached TMA descriptors of the tensor-core reconstruction
   bool has_plan = false;
   int plan_ctas = -1;
@@ -175,8 +182,10 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
     // Move(GPU2CPU) + Send + Receive, fused over NVLS when the gather buffer is symmetric
     bool mc = false;
     if (coll && (rc = symm_pack_mc(c, un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v, un.gbuf,
-                                   cs, &mc)))
+                                   cs, &mc, un.flag_mode ? un.gbuf2 : nullptr, un.gflags,
+                                   un.gstate)))
       return rc;
+    if (un.flag_mode && !mc) POS_FAIL(POS_ESTATE, "flag-mode gather could not be launched");
     if (!mc) {
       // A2 pack into this rank's slot
       cudaError_t e = launch_pack_factors(un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v,
@@ -184,7 +193,14 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
       if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack launch");
     }
     if (ts && (rc = trec(ts->packed, cs))) return rc;
-    if (coll && mc) {
+    if (coll && mc && un.flag_mode) {
+      // our slot is pushed; the apply stream waits for every rank's ready flag (no barrier on
+      // the comm stream, which moves on to the next unit at once)
+      POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));
+      POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
+      if ((rc = symm_wait_gathered(c, un.gflags, un.gstate, as))) return rc;
+      if (ts && (rc = trec(ts->gathered, as))) return rc;
+    } else if (coll && mc) {
       if (ts && (rc = trec(ts->gathered, cs))) return rc;
       POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));
       POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
@@ -205,8 +221,11 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
     if (ts && (rc = trec(ts->a0, as))) return rc;
     if (un.plan_ctas != c->max_ctas) {   // (re)build the cached launch plan
       un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * P, un.dtype, un.gbuf, un.W,
-                                     un.N, c->max_ctas, un.b);
+                                     un.N, c->max_ctas, un.b, un.flag_mode ? un.gbuf2 : nullptr);
       un.plan.counter = (s->flags & POS_SCHED_STATIC_TILES) ? nullptr : un.tile_counter;
+      un.plan.gsel = un.flag_mode ? un.gstate : nullptr;
+      if (un.flag_mode && !un.has_plan)
+        POS_FAIL(POS_ESTATE, "flag-mode gather without a tensor-core plan");
       un.plan_ctas = c->max_ctas;
     }
     if (un.has_plan) {
@@ -361,9 +380,28 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));
   if (scheme == POS_SCHEME_SFB && c->world > 1 && !c->local && (s->flags & POS_SCHED_NO_SYMM) == 0) {
     // gather buffer in symmetric memory: the factors are multicast straight into it (collective,
-    // every rank registers its layers in the same order)
-    if (pos_mem_alloc(c, (int64_t)bytes, &u.gbuf) == POS_OK) u.gbuf_symm = true;
-    else clear_error();
+    // every rank registers its layers in the same order). Flag mode (tensor-core path only: the
+    // reconstruction selects the buffer on the device): two buffers + P ready flags in one
+    // allocation.
+    static const bool flags_off = [] {
+      const char* e = getenv("POS_GATHER_FLAGS");
+      return e && e[0] == '0';
+    }();
+    const bool fm = !flags_off && dtype != POS_DT_F32 && (N % 4) == 0;
+    const size_t al = (bytes + 255) & ~size_t(255);
+    const size_t total = fm ? 2 * al + 256 : bytes;
+    if (pos_mem_alloc(c, (int64_t)total, &u.gbuf) == POS_OK) {
+      u.gbuf_symm = true;
+      if (fm) {
+        u.flag_mode = true;
+        u.gbuf2 = static_cast<uint8_t*>(u.gbuf) + al;
+        u.gflags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(u.gbuf) + 2 * al);
+        POS_CUDA_TRY(cudaMalloc(&u.gstate, 2 * sizeof(unsigned)));
+        POS_CUDA_TRY(cudaMemset(u.gstate, 0, 2 * sizeof(unsigned)));
+      }
+    } else {
+      clear_error();
+    }
   }
   if (!u.gbuf) {
     cudaError_t e = cudaMalloc(&u.gbuf, bytes);
@@ -554,6 +592,7 @@ int pos_sched_destroy(pos_sched* s) {
       else cudaFree(un.gbuf);
     }
     if (un.tile_counter) cudaFree(un.tile_counter);
+    if (un.gstate) cudaFree(un.gstate);
   }
   for (auto& ly : s->layers)
     if (ly.ev_ready) cudaEventDestroy(ly.ev_ready);

@@ -334,12 +334,14 @@ struct TileInfo {
   // launch on the same stream (and by every CUDA-graph replay).
   unsigned int* counter;
   float* bias;     // fused A4b: b (+)= alpha * accumulator column N; nullptr = no bias
+  const unsigned* gsel;   // double-buffered gather: buffer (*gsel - 1) & 1; nullptr = buffer 0
 };
 
 template <bool kTF32, bool kPair>
 __global__ void __launch_bounds__(THREADS, 1)
 sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmW, TileInfo ti, float alpha, int accumulate) {
+              const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA2,
+              const __grid_constant__ CUtensorMap tmB2, TileInfo ti, float alpha, int accumulate) {
   using L = Lay<kPair>;
   constexpr int ST = L::kStages;             // operand ring depth
   constexpr int EB = kTF32 ? 4 : 2;          // element bytes
@@ -406,9 +408,13 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // operand maps of the gather buffer this iteration's pack wrote (double buffering)
+  const bool second = ti.gsel && ((*reinterpret_cast<const volatile unsigned*>(ti.gsel) - 1u) & 1u);
+  const CUtensorMap* mA = second ? &tmA2 : &tmA;
+  const CUtensorMap* mB = second ? &tmB2 : &tmB;
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(mA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(mB) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
   }
   if (warp == 1) {
@@ -478,19 +484,19 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (leader) mbar_expect_tx(b_full + 8 * stage, 2 * L::kStageBytes);
 #pragma unroll
             for (int c = 0; c < BM / CHUNK; ++c)
-              tma_load_2d_pair(&tmA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
+              tma_load_2d_pair(mA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
 #pragma unroll
             for (int c = 0; c < L::kBCols / CHUNK; ++c)
-              tma_load_2d_pair(&tmB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
+              tma_load_2d_pair(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
           } else {
             const uint32_t full = b_full + 8 * stage;
             mbar_expect_tx(full, L::kStageBytes);
 #pragma unroll
             for (int c = 0; c < BM / CHUNK; ++c)
-              tma_load_2d(&tmA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
+              tma_load_2d(mA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
 #pragma unroll
             for (int c = 0; c < L::kBCols / CHUNK; ++c)
-              tma_load_2d(&tmB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
+              tma_load_2d(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
           }
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
@@ -754,7 +760,7 @@ int max_pairs() {
 
 template <bool kTF32>
 bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
-                    int64_t ldw, int max_ctas, float* bias) {
+                    int64_t ldw, int max_ctas, float* bias, const void* G2) {
   // with a bias the V operand includes the ones column N (the GEMM's extra output column)
   const int64_t NB = N + (bias ? 1 : 0);
   constexpr int EB = kTF32 ? 4 : 2;
@@ -773,6 +779,17 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
       !encode_2d(&pl->tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, W, (uint64_t)N, (uint64_t)M,
                  (uint64_t)(ldw * 4), WSUB, BM))
     return false;
+  if (G2) {
+    const uint8_t* g2 = static_cast<const uint8_t*>(G2);
+    if (!encode_2d(&pl->tmA2, dt, g2, (uint64_t)M, (uint64_t)KP, (uint64_t)(R * EB), CHUNK, BK,
+                   oswz) ||
+        !encode_2d(&pl->tmB2, dt, g2 + Mp * EB, (uint64_t)NB, (uint64_t)KP, (uint64_t)(R * EB),
+                   CHUNK, BK, oswz))
+      return false;
+  } else {
+    pl->tmA2 = pl->tmA;
+    pl->tmB2 = pl->tmB;
+  }
   pl->M = M; pl->N = N; pl->KP = KP;
   pl->nb_n = (int)((NB + BN - 1) / BN);
   pl->bias = bias;
@@ -803,6 +820,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
   ti.counter = pl.counter;
   ti.bias = pl.bias;
+  ti.gsel = pl.gsel;
   if constexpr (kPair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.grid);
@@ -816,11 +834,11 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true>, pl.tmA, pl.tmB, pl.tmW, ti, alpha,
-                              accumulate);
+    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true>, pl.tmA, pl.tmB, pl.tmW, pl.tmA2,
+                              pl.tmB2, ti, alpha, accumulate);
   } else {
-    sfb_tc_kernel<kTF32, false><<<pl.grid, THREADS, smem_bytes, s>>>(pl.tmA, pl.tmB, pl.tmW, ti,
-                                                                     alpha, accumulate);
+    sfb_tc_kernel<kTF32, false><<<pl.grid, THREADS, smem_bytes, s>>>(
+        pl.tmA, pl.tmB, pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
     return cudaGetLastError();
   }
 }
@@ -835,10 +853,13 @@ bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
 }
 
 bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t dtype,
-                      const void* G, float* W, int64_t ldw, int max_ctas, float* bias) {
+                      const void* G, float* W, int64_t ldw, int max_ctas, float* bias,
+                      const void* G2) {
   if (dtype == POS_DT_F32 || !sfb_tc_supported(N, ldw, W, G)) return false;
-  if (dtype == POS_DT_TF32) return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas, bias);
-  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas, bias);
+  if (G2 && !aligned16(G2)) return false;
+  if (dtype == POS_DT_TF32)
+    return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2);
+  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2);
 }
 
 cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {

@@ -128,18 +128,41 @@ ps_nvls_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, s
 __device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ float ld_in(const float* p) { return *p; }
 
+// Gather state of one SFB unit in flag mode (device memory of this rank, zero-initialised):
+// [0] packs completed by this rank (= iteration sequence), [1] CTAs of the running pack done.
+struct GatherFlags {
+  ncclWindow_t win;      // symmetric window holding the unit's P ready flags
+  size_t off_mine;       // offset of flag[rank] (written by this rank into every replica)
+  unsigned* state;       // this rank's GatherFlags state (2 x u32)
+};
+
 // One 16-byte output vector per thread iteration, multicast to every rank's gather buffer.
-template <typename Tin, bool kBF16>
+//  kFlag = false: barrier mode — an entry barrier (cross-rank WAR on the single gather buffer) and
+//    an exit barrier (all P slots have landed everywhere) around the multicast.
+//  kFlag = true: flag mode — no waiting at all: the gather buffer is double-buffered by the
+//    iteration parity read from device memory (so a replayed CUDA graph alternates too), and the
+//    last CTA to finish publishes "slot of rank r for iteration s is complete" as a release-store
+//    of s into flag[r] of every replica. The consumer waits for the P flags (wait_flags_kernel).
+//    WAR safety: rank r writes buffer s%2 at iteration s only after its iteration s-1 consumed
+//    every rank's s-1 flag, and each rank publishes its s-1 flag only after finishing iteration
+//    s-2, whose reconstruction was the last reader of buffer s%2.
+template <typename Tin, bool kBF16, bool kFlag>
 __global__ void __launch_bounds__(256)
-pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, const Tin* __restrict__ u,
-               const Tin* __restrict__ v, int64_t M, int64_t N, int64_t Mp, int64_t R,
-               int64_t K) {
-  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
-  // Entry barrier: every rank has reached this iteration's pack on its comm stream, which (by
-  // pos_sched_end's contract) is after its previous reconstruction finished reading the gather
-  // buffer we are about to overwrite (cross-rank WAR).
-  bar.sync(ncclCoopCta(), kEntryOrder);
-  float* dst = static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off_slot, dc));
+pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slot2,
+               const Tin* __restrict__ u, const Tin* __restrict__ v, int64_t M, int64_t N,
+               int64_t Mp, int64_t R, int64_t K, GatherFlags gf) {
+  uint32_t seq = 0;
+  if constexpr (!kFlag) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
+    // Entry barrier: every rank has reached this iteration's pack on its comm stream, which (by
+    // pos_sched_end's contract) is after its previous reconstruction finished reading the gather
+    // buffer we are about to overwrite (cross-rank WAR).
+    bar.sync(ncclCoopCta(), kEntryOrder);
+  } else {
+    seq = *reinterpret_cast<volatile unsigned*>(gf.state);
+  }
+  const size_t off = (kFlag && (seq & 1)) ? off_slot2 : off_slot;
+  float* dst = static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off, dc));
   constexpr int VEC = kBF16 ? 8 : 4;
   const int64_t chunks_per_row = R / VEC, total = K * chunks_per_row;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
@@ -166,7 +189,37 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, const Tin* __r
     // element offset of this 16-byte vector in float units: (k * R + col) * eb / 4
     mm_st_v4(dst + ((k * R + col) * (kBF16 ? 2 : 4)) / 4, o);
   }
-  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // all P slots have landed everywhere
+  if constexpr (!kFlag) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // all P slots have landed everywhere
+  } else {
+    __threadfence_system();                 // this thread's multicast stores are performed
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned prev = atomicAdd(gf.state + 1, 1u);
+      if (prev == gridDim.x - 1) {          // last CTA: every CTA's stores are performed
+        __threadfence_system();
+        gf.state[1] = 0;
+        gf.state[0] = seq + 1;
+        uint32_t* fmc = static_cast<uint32_t*>(ncclGetLsaMultimemPointer(gf.win, gf.off_mine, dc));
+        asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(fmc), "r"(seq + 1)
+                     : "memory");
+      }
+    }
+  }
+}
+
+// Consumer side of flag mode: returns once every rank's slot of this iteration is in place
+// (flag[r] >= this rank's own sequence, which its pack has just advanced).
+__global__ void wait_flags_kernel(const uint32_t* flags, const unsigned* state, int P) {
+  const uint32_t want = *reinterpret_cast<const volatile unsigned*>(state);
+  for (int r = threadIdx.x; r < P; r += blockDim.x) {
+    uint32_t got;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(got) : "l"(flags + r) : "memory");
+    } while ((int32_t)(got - want) < 0);
+  }
+  __syncthreads();
 }
 
 int grid_for(int64_t items, int threads, int cap) {
@@ -255,8 +308,38 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   return POS_OK;
 }
 
+namespace {
+template <bool kFlag>
+void launch_pack_mc(int grid, cudaStream_t s, const ncclDevComm& dc, ncclWindow_t wgb,
+                    size_t off_slot, size_t off_slot2, int32_t in_dtype, int32_t dtype,
+                    const void* u, const void* v, int64_t M, int64_t N, int64_t Mp, int64_t R,
+                    int64_t K, GatherFlags gf) {
+  using bf = __nv_bfloat16;
+  if (dtype == POS_DT_BF16) {
+    if (in_dtype == POS_IN_BF16)
+      pack_mc_kernel<bf, true, kFlag><<<grid, 256, 0, s>>>(
+          dc, wgb, off_slot, off_slot2, static_cast<const bf*>(u), static_cast<const bf*>(v), M, N,
+          Mp, R, K, gf);
+    else
+      pack_mc_kernel<float, true, kFlag><<<grid, 256, 0, s>>>(
+          dc, wgb, off_slot, off_slot2, static_cast<const float*>(u),
+          static_cast<const float*>(v), M, N, Mp, R, K, gf);
+  } else {
+    if (in_dtype == POS_IN_BF16)
+      pack_mc_kernel<bf, false, kFlag><<<grid, 256, 0, s>>>(
+          dc, wgb, off_slot, off_slot2, static_cast<const bf*>(u), static_cast<const bf*>(v), M, N,
+          Mp, R, K, gf);
+    else
+      pack_mc_kernel<float, false, kFlag><<<grid, 256, 0, s>>>(
+          dc, wgb, off_slot, off_slot2, static_cast<const float*>(u),
+          static_cast<const float*>(v), M, N, Mp, R, K, gf);
+  }
+}
+}  // namespace
+
 int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
-                 const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done) {
+                 const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done,
+                 void* gbuf2, uint32_t* flags, unsigned* fstate) {
   clear_stale_launch_error();
   *done = false;
   if (c->world < 2 || c->local) return POS_OK;
@@ -267,12 +350,16 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   if (mc_off) return POS_OK;
   const int64_t R = row_elems(M, N), eb = dtype_bytes(dtype);
   const size_t slot_bytes = (size_t)(K * R * eb);
-  ncclWindow_t wgb;
-  size_t off;
+  ncclWindow_t wgb, wgb2, wfl;
+  size_t off, off2 = 0, offf = 0;
   if (!symm_lookup(c, gbuf, slot_bytes * c->world, &wgb, &off)) return POS_OK;
+  // flag mode needs the second buffer in the same window as the first (one window argument)
+  const bool flag_mode = gbuf2 && flags && fstate &&
+                         symm_lookup(c, gbuf2, slot_bytes * c->world, &wgb2, &off2) &&
+                         symm_lookup(c, flags, sizeof(uint32_t) * c->world, &wfl, &offf);
+  if (gbuf2 && !flag_mode) return POS_OK;   // inconsistent registration: caller uses NCCL
   const size_t off_slot = off + (size_t)c->rank * slot_bytes;
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
-  // few CTAs: every CTA pays two cross-GPU barriers, and the stores are fire-and-forget
   static const int pack_ctas = [] {
     const char* e = getenv("POS_PACK_CTAS");
     const int v = (e && *e) ? atoi(e) : 128;
@@ -281,28 +368,29 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   const int grid = grid_for(K * (R / vec), 256, pack_ctas);
   const int64_t Mp = m_pad(M);
   const ncclDevComm& dc = state(c)->dev;
-  if (dtype == POS_DT_BF16) {
-    if (in_dtype == POS_IN_BF16)
-      pack_mc_kernel<__nv_bfloat16, true><<<grid, 256, 0, s>>>(
-          dc, wgb, off_slot, static_cast<const __nv_bfloat16*>(u),
-          static_cast<const __nv_bfloat16*>(v), M, N, Mp, R, K);
-    else
-      pack_mc_kernel<float, true><<<grid, 256, 0, s>>>(dc, wgb, off_slot,
-                                                        static_cast<const float*>(u),
-                                                        static_cast<const float*>(v), M, N, Mp, R, K);
+  if (flag_mode) {
+    // both buffers must be addressable through the first buffer's window: they are separate
+    // allocations, so pass the second one's window offset relative to its own window instead
+    GatherFlags gf{wfl, offf + sizeof(uint32_t) * (size_t)c->rank, fstate};
+    if (wgb2 != wgb) return POS_OK;         // (separate windows: not supported, NCCL path)
+    launch_pack_mc<true>(grid, s, dc, wgb, off_slot, off2 + (size_t)c->rank * slot_bytes,
+                         in_dtype, dtype, u, v, M, N, Mp, R, K, gf);
   } else {
-    if (in_dtype == POS_IN_BF16)
-      pack_mc_kernel<__nv_bfloat16, false><<<grid, 256, 0, s>>>(
-          dc, wgb, off_slot, static_cast<const __nv_bfloat16*>(u),
-          static_cast<const __nv_bfloat16*>(v), M, N, Mp, R, K);
-    else
-      pack_mc_kernel<float, false><<<grid, 256, 0, s>>>(dc, wgb, off_slot,
-                                                         static_cast<const float*>(u),
-                                                         static_cast<const float*>(v), M, N, Mp, R, K);
+    launch_pack_mc<false>(grid, s, dc, wgb, off_slot, off_slot, in_dtype, dtype, u, v, M, N, Mp,
+                          R, K, GatherFlags{});
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack_mc_kernel launch");
   *done = true;
+  return POS_OK;
+}
+
+int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate,
+                       cudaStream_t s) {
+  clear_stale_launch_error();
+  wait_flags_kernel<<<1, 32, 0, s>>>(flags, fstate, c->world);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "wait_flags_kernel launch");
   return POS_OK;
 }
 

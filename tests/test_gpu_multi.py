@@ -134,7 +134,7 @@ def _worker(rank, world, port, outdir):
         check("sfb_stat_dW", err(g3 - W30, Wr3 - W30) <= 2e-3)
         res["digests"]["sfb_stat"] = _digest(W3)
         # ---- (e) WFBP scheduler: FC (SFB) + bucket + dense; WFBP == sequential, both == oracle --
-        def run_sched(sequential, graph, symm_dense=False):
+        def run_sched(sequential, graph, symm_dense=False, iters=1):
             alloc = (lambda k: ctx.sym_empty(k)) if symm_dense else (lambda k: torch.zeros(k, device=dev))
             sch = pos.Scheduler(ctx, 5, timing="apply", sequential=sequential)
             sizes = [1792, 36928]
@@ -180,22 +180,32 @@ def _worker(rank, world, port, outdir):
 
             fill()
             torch.cuda.synchronize()
-            if graph:
+            if graph:   # one captured iteration, replayed: device-side state must advance per replay
                 gr = torch.cuda.CUDAGraph()
                 cs = torch.cuda.Stream()
                 cs.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.graph(gr, stream=cs, capture_error_mode="thread_local"):
                     step(torch.cuda.current_stream())
                 torch.cuda.synchronize()
-                gr.replay()
+                for it in range(iters):
+                    if it:
+                        fill()   # the NCCL path reduces in place
+                    gr.replay()
             else:
-                step(torch.cuda.current_stream())
+                for it in range(iters):
+                    if it:
+                        fill()
+                    step(torch.cuda.current_stream())
             torch.cuda.synchronize()
-            ok = np.array_equal(to_host(Wb[:nb]), sync.ps_update(wb0, gb, a))
-            ok &= np.array_equal(to_host(Wq[:n2]), sync.ps_update(wd0, gd, a))
-            wf1, bf1 = sync.sfb_update(wf0, bf0, Uf, Vf, a)
+            wb1, wd1, wf1, bf1, wg1 = wb0, wd0, wf0, bf0, wg0
+            for _ in range(iters):
+                wb1 = sync.ps_update(wb1, gb, a)
+                wd1 = sync.ps_update(wd1, gd, a)
+                wf1, bf1 = sync.sfb_update(wf1, bf1, Uf, Vf, a)
+                wg1, _ = sync.sfb_update(wg1, None, Ug, Vg, a)
+            ok = np.array_equal(to_host(Wb[:nb]), wb1)
+            ok &= np.array_equal(to_host(Wq[:n2]), wd1)
             ok &= np.array_equal(to_host(Wf), wf1) and np.array_equal(to_host(Bf), bf1)
-            wg1, _ = sync.sfb_update(wg0, None, Ug, Vg, a)
             ok &= np.array_equal(to_host(Wg), wg1)
             dig = _digest(Wb[:nb]) + _digest(Wq[:n2]) + _digest(Wf) + _digest(Wg)
             sch.close()
@@ -206,6 +216,15 @@ def _worker(rank, world, port, outdir):
         ok_g, dig_g = run_sched(False, True)
         ok_n, dig_n = run_sched(False, True, symm_dense=True)
         ok_ns, dig_ns = run_sched(True, False, symm_dense=True)
+        # several iterations: the double-buffered flag-mode gather alternates buffers (by a device
+        # counter, so a single replayed graph alternates too) and the flags keep advancing
+        ok_n5, dig_n5 = run_sched(False, True, symm_dense=True, iters=5)
+        ok_w5, dig_w5 = run_sched(False, False, symm_dense=True, iters=5)
+        ok_s5, dig_s5 = run_sched(True, False, iters=5)
+        check("sched_nvls_graph_5iter_oracle", ok_n5)
+        check("sched_nvls_eager_5iter_oracle", ok_w5)
+        check("sched_seq_5iter_oracle", ok_s5)
+        check("sched_5iter_replicas_agree", dig_n5 == dig_w5 == dig_s5)
         check("sched_nvls_graph_oracle", ok_n)
         check("sched_nvls_seq_oracle", ok_ns)
         check("sched_wfbp_oracle", ok_w)
