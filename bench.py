@@ -485,10 +485,16 @@ def run_ours(a):
             "step": {"t_roofline_pipelined_ms": t_pipe * 1e3, "t_roofline_sequential_ms": t_seq * 1e3,
                      "t_nvlink_ms": t_nvl * 1e3, "t_kernels_ms": t_kern * 1e3,
                      "frac_pipelined": (t_pipe * 1e3) / ms, "nvlink_gbs_per_dir": NVLINK_GBS_PER_DIR}}
+    symm_on = P > 1 and not a.no_symm
+    flags_on = symm_on and os.environ.get("POS_GATHER_FLAGS", "1") != "0" and a.dtype != "f32"
     n_launch = 0
     for r, un in zip(rows, units):
         if r["scheme"] == "SFB":
-            n_launch += 3                   # pack, reconstruct-and-apply, bias
+            # P = 1: pack + reconstruct-and-apply (bias fused); P > 1 (NVLS): multicast pack +
+            # reconstruct, plus the ready-flag wait kernel in flag mode; NCCL path: + all-gather
+            n_launch += 2 + (1 if flags_on else 0)
+        elif symm_on:
+            n_launch += 1                   # fused NVLS reduce + apply + multicast kernel
         else:
             lo, hi = pos.pos_shard_range(un["n"], P, rank)
             ln = hi - lo

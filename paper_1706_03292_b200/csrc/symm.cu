@@ -146,11 +146,13 @@ struct GatherFlags {
 //    WAR safety: rank r writes buffer s%2 at iteration s only after its iteration s-1 consumed
 //    every rank's s-1 flag, and each rank publishes its s-1 flag only after finishing iteration
 //    s-2, whose reconstruction was the last reader of buffer s%2.
-template <typename Tin, bool kBF16, bool kFlag>
+//  kUC (flag mode only): P unicast stores through the peers' LSA pointers instead of one
+//    multimem store (an experiment knob, POS_PACK_UC=1).
+template <typename Tin, bool kBF16, bool kFlag, bool kUC = false>
 __global__ void __launch_bounds__(256)
 pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slot2,
                const Tin* __restrict__ u, const Tin* __restrict__ v, int64_t M, int64_t N,
-               int64_t Mp, int64_t R, int64_t K, GatherFlags gf) {
+               int64_t Mp, int64_t R, int64_t K, GatherFlags gf, int P = 0) {
   uint32_t seq = 0;
   if constexpr (!kFlag) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
@@ -162,7 +164,10 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slo
     seq = *reinterpret_cast<volatile unsigned*>(gf.state);
   }
   const size_t off = (kFlag && (seq & 1)) ? off_slot2 : off_slot;
-  float* dst = static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off, dc));
+  float* dst = kUC ? nullptr : static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off, dc));
+  float* peer_dst[8];
+  if constexpr (kUC)
+    for (int p = 0; p < P && p < 8; ++p) peer_dst[p] = static_cast<float*>(ncclGetLsaPointer(wgb, off, p));
   constexpr int VEC = kBF16 ? 8 : 4;
   const int64_t chunks_per_row = R / VEC, total = K * chunks_per_row;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
@@ -187,7 +192,12 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slo
       o.w = idx + 3 < lim ? ld_in(src + idx + 3) : (idx + 3 == onec ? 1.f : 0.f);
     }
     // element offset of this 16-byte vector in float units: (k * R + col) * eb / 4
-    mm_st_v4(dst + ((k * R + col) * (kBF16 ? 2 : 4)) / 4, o);
+    const int64_t eo = ((k * R + col) * (kBF16 ? 2 : 4)) / 4;
+    if constexpr (kUC) {
+      for (int p = 0; p < P && p < 8; ++p) *reinterpret_cast<float4*>(peer_dst[p] + eo) = o;
+    } else {
+      mm_st_v4(dst + eo, o);
+    }
   }
   if constexpr (!kFlag) {
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
@@ -201,9 +211,17 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slo
         __threadfence_system();
         gf.state[1] = 0;
         gf.state[0] = seq + 1;
-        uint32_t* fmc = static_cast<uint32_t*>(ncclGetLsaMultimemPointer(gf.win, gf.off_mine, dc));
-        asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(fmc), "r"(seq + 1)
-                     : "memory");
+        if constexpr (kUC) {
+          for (int p = 0; p < P && p < 8; ++p) {
+            uint32_t* f = static_cast<uint32_t*>(ncclGetLsaPointer(gf.win, gf.off_mine, p));
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(seq + 1) : "memory");
+          }
+        } else {
+          uint32_t* fmc =
+              static_cast<uint32_t*>(ncclGetLsaMultimemPointer(gf.win, gf.off_mine, dc));
+          asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(fmc), "r"(seq + 1)
+                       : "memory");
+        }
       }
     }
   }
@@ -309,30 +327,30 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
 }
 
 namespace {
-template <bool kFlag>
+template <bool kFlag, bool kUC = false>
 void launch_pack_mc(int grid, cudaStream_t s, const ncclDevComm& dc, ncclWindow_t wgb,
                     size_t off_slot, size_t off_slot2, int32_t in_dtype, int32_t dtype,
                     const void* u, const void* v, int64_t M, int64_t N, int64_t Mp, int64_t R,
-                    int64_t K, GatherFlags gf) {
+                    int64_t K, GatherFlags gf, int P = 0) {
   using bf = __nv_bfloat16;
   if (dtype == POS_DT_BF16) {
     if (in_dtype == POS_IN_BF16)
-      pack_mc_kernel<bf, true, kFlag><<<grid, 256, 0, s>>>(
+      pack_mc_kernel<bf, true, kFlag, kUC><<<grid, 256, 0, s>>>(
           dc, wgb, off_slot, off_slot2, static_cast<const bf*>(u), static_cast<const bf*>(v), M, N,
-          Mp, R, K, gf);
+          Mp, R, K, gf, P);
     else
-      pack_mc_kernel<float, true, kFlag><<<grid, 256, 0, s>>>(
+      pack_mc_kernel<float, true, kFlag, kUC><<<grid, 256, 0, s>>>(
           dc, wgb, off_slot, off_slot2, static_cast<const float*>(u),
-          static_cast<const float*>(v), M, N, Mp, R, K, gf);
+          static_cast<const float*>(v), M, N, Mp, R, K, gf, P);
   } else {
     if (in_dtype == POS_IN_BF16)
-      pack_mc_kernel<bf, false, kFlag><<<grid, 256, 0, s>>>(
+      pack_mc_kernel<bf, false, kFlag, kUC><<<grid, 256, 0, s>>>(
           dc, wgb, off_slot, off_slot2, static_cast<const bf*>(u), static_cast<const bf*>(v), M, N,
-          Mp, R, K, gf);
+          Mp, R, K, gf, P);
     else
-      pack_mc_kernel<float, false, kFlag><<<grid, 256, 0, s>>>(
+      pack_mc_kernel<float, false, kFlag, kUC><<<grid, 256, 0, s>>>(
           dc, wgb, off_slot, off_slot2, static_cast<const float*>(u),
-          static_cast<const float*>(v), M, N, Mp, R, K, gf);
+          static_cast<const float*>(v), M, N, Mp, R, K, gf, P);
   }
 }
 }  // namespace
@@ -373,8 +391,16 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
     // allocations, so pass the second one's window offset relative to its own window instead
     GatherFlags gf{wfl, offf + sizeof(uint32_t) * (size_t)c->rank, fstate};
     if (wgb2 != wgb) return POS_OK;         // (separate windows: not supported, NCCL path)
-    launch_pack_mc<true>(grid, s, dc, wgb, off_slot, off2 + (size_t)c->rank * slot_bytes,
-                         in_dtype, dtype, u, v, M, N, Mp, R, K, gf);
+    static const bool uc = [] {
+      const char* e = getenv("POS_PACK_UC");
+      return e && e[0] == '1';
+    }();
+    if (uc && c->world <= 8)
+      launch_pack_mc<true, true>(grid, s, dc, wgb, off_slot, off2 + (size_t)c->rank * slot_bytes,
+                                 in_dtype, dtype, u, v, M, N, Mp, R, K, gf, c->world);
+    else
+      launch_pack_mc<true>(grid, s, dc, wgb, off_slot, off2 + (size_t)c->rank * slot_bytes,
+                           in_dtype, dtype, u, v, M, N, Mp, R, K, gf);
   } else {
     launch_pack_mc<false>(grid, s, dc, wgb, off_slot, off_slot, in_dtype, dtype, u, v, M, N, Mp,
                           R, K, GatherFlags{});
