@@ -359,6 +359,10 @@ def run_ours(a):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # span of the reconstructions within the step (they overlap: two streams) — before timing(),
+    # which retires the events in eager mode
+    a4_span_ms = sch.timing_span(pos.POS_SCHEME_SFB) if any(
+        u["kind"] == "fc" for u in units) else None
     unit_times = [sch.timing(un["layers"][0]) for un in units]
     # clock soak: if the timed region was too short for the 50 ms sampler, keep the same load
     # running (untimed) for ~1 s so the clock record describes this workload under load
@@ -459,7 +463,8 @@ def run_ours(a):
     t_pipe, t_seq, t_nvl, t_kern = roofline_times(rows, peaks, P)
     a4_bytes = sum(r["hbm_a4"] for r in rows)
     a4_flop = sum(r["flop_a4"] for r in rows)
-    a4_ms = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "SFB")
+    a4_ms_sum = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "SFB")
+    a4_ms = a4_span_ms if a4_span_ms else a4_ms_sum
     ps_bytes = sum(r["hbm_other"] for r in rows if r["scheme"] == "PS")
     ps_ms = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "PS")
     traffic = None
@@ -476,6 +481,9 @@ def run_ours(a):
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic,
             "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
+            "kernel_ms_note": "span from the first reconstruction's start to the last one's end in "
+                              "a step (consecutive layers' reconstructions overlap on two streams); "
+                              "sum of per-layer durations: %.4f ms" % a4_ms_sum,
             "peak_source": peaks["source"],
             "tensor_tflops": a4_flop / (a4_ms / 1e3) / 1e12 if a4_ms > 0 else None,
             "tensor_frac_of_bf16_peak": (a4_flop / (a4_ms / 1e3) / 1e12) / peaks["bf16_tflops"] if a4_ms > 0 else None,

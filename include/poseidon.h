@@ -255,6 +255,14 @@ int pos_sched_scheme(pos_sched* s, int32_t l);
  * runs it. Synchronises on the layer's outstanding iterations. Returns the iteration count (> 0). */
 int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, float* apply_ms);
 int pos_sched_timing_reset(pos_sched* s);
+/* With POS_SCHED_TIMING(_APPLY): the device-time SPAN (earliest apply start to latest apply end)
+ * of all units of `scheme` (POS_SCHEME_SFB or POS_SCHEME_PS) within one iteration, averaged over
+ * the (up to 4) most recent iterations whose timing events are still live. Reconstructions of
+ * different layers may overlap (they alternate between two streams), so this — not the sum of
+ * per-layer apply times — is the time the step spends in them. Call it before pos_sched_timing
+ * in eager mode (which retires the events). Returns the number of iterations averaged (> 0);
+ * POS_ESTATE if none is available. */
+int pos_sched_timing_span(pos_sched* s, int32_t scheme, float* span_ms);
 int pos_sched_destroy(pos_sched* s);
 
 #ifdef __cplusplus

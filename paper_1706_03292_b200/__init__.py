@@ -296,6 +296,14 @@ class Scheduler:
     def timing_reset(self):
         _chk(lib().pos_sched_timing_reset(self.h), "pos_sched_timing_reset")
 
+    def timing_span(self, scheme=None):
+        """Device ms from the earliest to the latest apply of all units of `scheme` (default SFB)
+        in one iteration, averaged over the live timing slots (pos_sched_timing_span)."""
+        sp = C.c_float()
+        _chk(lib().pos_sched_timing_span(self.h, POS_SCHEME_SFB if scheme is None else scheme,
+                                         C.byref(sp)), "pos_sched_timing_span")
+        return sp.value
+
     def close(self):
         if self.h:
             lib().pos_sched_destroy(self.h)

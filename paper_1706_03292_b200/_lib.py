@@ -57,6 +57,7 @@ SIGNATURES = {
     "pos_sched_scheme": (C.c_int, [vp, i32]),
     "pos_sched_timing": (C.c_int, [vp, i32, P_f32, P_f32, P_f32]),
     "pos_sched_timing_reset": (C.c_int, [vp]),
+    "pos_sched_timing_span": (C.c_int, [vp, i32, P_f32]),
     "pos_sched_destroy": (C.c_int, [vp]),
 }
 

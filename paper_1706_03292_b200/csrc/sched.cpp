@@ -28,7 +28,7 @@
 
 namespace {
 
-constexpr int kPool = 4;    // apply streams
+constexpr int kPool = 5;    // apply streams: [0], [4] reconstructions; [1..3] dense applies
 constexpr int kTRing = 4;   // timing event sets per unit (iterations in flight)
 
 struct TSlot {
@@ -67,6 +67,7 @@ struct Unit {
   double acc_pack = 0, acc_comm = 0, acc_apply = 0;
   int64_t n_acc = 0;
   int seq = 0;                 // registration order (stream assignment)
+  int sfb_idx = 0;             // index among the SFB units (reconstruction stream assignment)
 };
 
 struct Layer {
@@ -95,6 +96,8 @@ struct pos_sched {
   bool captured = false;   // some iteration was issued under CUDA-graph stream capture
   int last_sfb = -1;       // most recently issued SFB unit of this iteration
   bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
+  int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1: one, in order)
+  int n_sfb = 0;              // SFB units registered
 };
 
 using namespace pos;
@@ -163,10 +166,15 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
     ts->used = true;
   }
   // stream of the first stage: the comm stream when a collective follows, else an apply stream
-  cudaStream_t as = un.scheme == POS_SCHEME_SFB ? s->pool[0] : s->pool[1 + un.seq % (kPool - 1)];
+  // Consecutive SFB reconstructions alternate between two streams: they touch different layers, so
+  // the next one's CTAs can take each SM as the previous one's persistent CTAs leave (no
+  // full-drain gap between them); dense applies rotate over three more streams.
+  cudaStream_t as = un.scheme == POS_SCHEME_SFB
+                        ? s->pool[(s->sfb_streams > 1 && (un.sfb_idx & 1)) ? 4 : 0]
+                        : s->pool[1 + un.seq % 3];
   // first stage: the comm stream when a collective follows; else an auxiliary apply stream, so the
   // factor pack of the next SFB layer overlaps the reconstruction of this one
-  cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % (kPool - 1)];
+  cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % 3];
   for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_ready, 0));
   // Optionally keep the NVLink-latency-bound PS kernels from co-running with the HBM-bound
   // reconstructions (they starve each other's memory pipelines); see DESIGN.md.
@@ -331,6 +339,7 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   s->L = n_layers;
   s->flags = flags;
   s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
+  if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = atoi(e) > 1 ? 2 : 1;
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
   int lo = 0, hi = 0;
@@ -376,6 +385,7 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   u.in_dtype = in_dtype; u.dtype = dtype;
   u.W = W; u.b = b; u.grad = grad;
   u.members = {l};
+  if (scheme == POS_SCHEME_SFB) u.sfb_idx = s->n_sfb++;
   const int64_t rows = scheme == POS_SCHEME_SFB ? K * c->world : K;
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));
   if (scheme == POS_SCHEME_SFB && c->world > 1 && !c->local && (s->flags & POS_SCHED_NO_SYMM) == 0) {
@@ -548,6 +558,44 @@ int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, fl
   if (comm_ms) *comm_ms = (float)(un.acc_comm / un.n_acc);
   if (apply_ms) *apply_ms = (float)(un.acc_apply / un.n_acc);
   return (int)(un.n_acc > INT32_MAX ? INT32_MAX : un.n_acc);
+}
+
+int pos_sched_timing_span(pos_sched* s, int32_t scheme, float* span_ms) {
+  clear_error();
+  POS_CHECK_ARG(s && span_ms, "bad arguments");
+  POS_CHECK_ARG(scheme == POS_SCHEME_SFB || scheme == POS_SCHEME_PS, "bad scheme %d", scheme);
+  if (!timing_any(s)) POS_FAIL(POS_ESTATE, "scheduler created without timing");
+  double acc = 0;
+  int n = 0;
+  for (int t = 0; t < kTRing; ++t) {
+    const TSlot* ref = nullptr;
+    bool all = true, any = false;
+    for (auto& un : s->units) {
+      if (un.scheme != scheme) continue;
+      any = true;
+      if (!un.ring[t].used) { all = false; break; }
+      if (!ref) ref = &un.ring[t];
+    }
+    if (!any || !all) continue;
+    float lo = 0, hi = 0;
+    bool first = true;
+    for (auto& un : s->units) {
+      if (un.scheme != scheme) continue;
+      const TSlot& ts = un.ring[t];
+      POS_CUDA_TRY(cudaEventSynchronize(ts.a1));
+      float a0 = 0, a1 = 0;
+      POS_CUDA_TRY(cudaEventElapsedTime(&a0, ref->a0, ts.a0));
+      POS_CUDA_TRY(cudaEventElapsedTime(&a1, ref->a0, ts.a1));
+      if (first || a0 < lo) lo = a0;
+      if (first || a1 > hi) hi = a1;
+      first = false;
+    }
+    acc += hi - lo;
+    ++n;
+  }
+  if (n == 0) POS_FAIL(POS_ESTATE, "no iteration with live timing events for scheme %d", scheme);
+  *span_ms = (float)(acc / n);
+  return n;
 }
 
 int pos_sched_timing_reset(pos_sched* s) {

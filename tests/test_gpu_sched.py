@@ -93,7 +93,11 @@ def run(model, alpha, sequential=False, timing=False, delay_cycles=0, static_til
                 sch.factors_ready(l, dev[l]["u"], dev[l]["v"], producer)
     sch.end(consumer)
     torch.cuda.synchronize()
+    span = sch.timing_span(pos.POS_SCHEME_SFB) if timing and any(
+        d["kind"] != "dense" and d.get("force") != pos.POS_SCHEME_PS for d in model) else None
     timings = [sch.timing(l) for l in range(len(model))] if timing else None
+    if timing:
+        timings = (timings, span)
     out = []
     for l, d in enumerate(model):
         if d["kind"] == "dense":
@@ -120,9 +124,13 @@ def test_sched_wfbp_matches_oracle_and_sequential_bitwise():
 
 def test_sched_timing_reports():
     model = make_model(2)
-    _, t, _ = run(model, si.EXACT_ALPHA, timing=True)
+    _, (t, span), _ = run(model, si.EXACT_ALPHA, timing=True)
     for pack, comm, apply in t:
         assert pack >= 0 and comm >= 0 and apply > 0
+    # the reconstructions' span covers the longest one (they may overlap on two streams)
+    sfb = [a for (p, c, a), d in zip(t, model) if d["kind"] != "dense" and d.get("force") != pos.POS_SCHEME_PS]
+    if span is not None:
+        assert span >= 0.99 * max(sfb)
 
 
 def test_sched_war_hazard_with_slow_backward():
