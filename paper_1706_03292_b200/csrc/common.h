@@ -89,6 +89,8 @@ cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const
                           int32_t accumulate, float* W, int64_t ldw, float* b, float alpha,
                           int max_ctas, cudaStream_t s);
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G);
+// the plan for inner dimension KP would use the CTA-pair (cluster) kernel
+bool sfb_tc_would_pair(int64_t KP);
 
 // A launch plan for the tensor-core reconstruct-and-apply: TMA descriptors encoded once for fixed
 // buffers (the scheduler keeps one per SFB layer, so the hot path does no host-side encoding).

@@ -98,6 +98,7 @@ struct pos_sched {
   bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
   int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1: one, in order)
   int n_sfb = 0;              // SFB units registered
+  bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
 };
 
 using namespace pos;
@@ -169,9 +170,12 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
   // Consecutive SFB reconstructions alternate between two streams: they touch different layers, so
   // the next one's CTAs can take each SM as the previous one's persistent CTAs leave (no
   // full-drain gap between them); dense applies rotate over three more streams.
-  cudaStream_t as = un.scheme == POS_SCHEME_SFB
-                        ? s->pool[(s->sfb_streams > 1 && (un.sfb_idx & 1)) ? 4 : 0]
-                        : s->pool[1 + un.seq % 3];
+  // Not with the CTA-pair (cluster) kernel: a cluster launch pending behind a running persistent
+  // kernel on another stream can hold SMs that the cross-GPU kernels need (observed deadlock at
+  // P = 4, AlexNet K*P = 512), so then all reconstructions stay on one stream.
+  const bool two = s->sfb_streams > 1 && !s->any_pair;
+  cudaStream_t as = un.scheme == POS_SCHEME_SFB ? s->pool[(two && (un.sfb_idx & 1)) ? 4 : 0]
+                                                : s->pool[1 + un.seq % 3];
   // first stage: the comm stream when a collective follows; else an auxiliary apply stream, so the
   // factor pack of the next SFB layer overlaps the reconstruction of this one
   cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % 3];
@@ -385,7 +389,10 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   u.in_dtype = in_dtype; u.dtype = dtype;
   u.W = W; u.b = b; u.grad = grad;
   u.members = {l};
-  if (scheme == POS_SCHEME_SFB) u.sfb_idx = s->n_sfb++;
+  if (scheme == POS_SCHEME_SFB) {
+    u.sfb_idx = s->n_sfb++;
+    if (dtype != POS_DT_F32 && sfb_tc_would_pair(K * c->world)) s->any_pair = true;
+  }
   const int64_t rows = scheme == POS_SCHEME_SFB ? K * c->world : K;
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));
   if (scheme == POS_SCHEME_SFB && c->world > 1 && !c->local && (s->flags & POS_SCHED_NO_SYMM) == 0) {

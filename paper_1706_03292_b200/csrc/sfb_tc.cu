@@ -845,6 +845,8 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
 
 }  // namespace
 
+bool sfb_tc_would_pair(int64_t KP) { return use_pair(KP); }
+
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
   // TMA stores move whole 16-byte chunks: the last W row chunk must not straddle column N (else
   // the element(s) after N in a strided W would be overwritten) -> N % 4 == 0 as well as ldw.
