@@ -21,10 +21,10 @@
 //  * the bias gradient comes out of the same GEMM: the packed v rows carry a 1.0 in column N,
 //    so accumulator column N is sum_j u_j (A4b fused; read with one tcgen05.ld 32x32b.x1).
 //
-//  * K*P >= 512: CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA
+//  * K*P >= 1024: CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA
 //    stages its 128 rows of U and half of the tile's V columns, the even CTA issues the MMAs
 //    for both; 1/3 less operand traffic and smaller stages (more in flight) where the operand
-//    stream, not W, is the bound. Measured (profiles/r01/README.md): +10% at K*P = 1024,
+//    stream, not W, is the bound. Measured (profiles/r01/README.md): +10% at K*P = 1024, +2% at 512,
 //    -2% at K*P <= 256 (the single-CTA kernel stays there).
 //
 // Warp roles (256 threads): w0 operand TMA producer, w1 MMA issuer + TMEM owner, w2 W TMA
@@ -706,7 +706,7 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 }
 
 #ifndef POS_SFB_PAIR_KP
-#define POS_SFB_PAIR_KP 512
+#define POS_SFB_PAIR_KP 1024
 #endif
 // CTA-pair kernel for K*P >= POS_SFB_PAIR_KP (env POS_SFB_PAIR=0|1 forces it off / on,
 // POS_SFB_PAIR_KP overrides the threshold; read at plan time).
