@@ -69,6 +69,9 @@ __device__ __forceinline__ void mm_st(float* p, float v) {
   asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+#ifndef POS_PACK_CTA_FENCE
+#define POS_PACK_CTA_FENCE 1
+#endif
 #ifndef POS_ENTRY_ORDER
 #define POS_ENTRY_ORDER cuda::memory_order_acquire
 #endif
@@ -203,8 +206,13 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slo
     ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // all P slots have landed everywhere
   } else {
+#if POS_PACK_CTA_FENCE
+    __syncthreads();                        // the CTA's stores happen-before thread 0's fence
+    if (threadIdx.x == 0) __threadfence_system();
+#else
     __threadfence_system();                 // this thread's multicast stores are performed
     __syncthreads();
+#endif
     if (threadIdx.x == 0) {
       const unsigned prev = atomicAdd(gf.state + 1, 1u);
       if (prev == gridDim.x - 1) {          // last CTA: every CTA's stores are performed
@@ -378,12 +386,20 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   if (gbuf2 && !flag_mode) return POS_OK;   // inconsistent registration: caller uses NCCL
   const size_t off_slot = off + (size_t)c->rank * slot_bytes;
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
+  // barrier mode: one LSA barrier index per CTA (<= kBarriers); flag mode: no barrier, more CTAs
+  // keep more multicast stores in flight
   static const int pack_ctas = [] {
     const char* e = getenv("POS_PACK_CTAS");
     const int v = (e && *e) ? atoi(e) : 128;
-    return v < 1 ? 1 : (v > kBarriers ? kBarriers : v);
+    return v < 1 ? 1 : v;
   }();
-  const int grid = grid_for(K * (R / vec), 256, pack_ctas);
+  static const int pack_ctas_flag = [] {
+    const char* e = getenv("POS_PACK_CTAS_FLAG");
+    const int v = (e && *e) ? atoi(e) : 128;
+    return v < 1 ? 1 : v;
+  }();
+  const int grid = grid_for(K * (R / vec), 256,
+                            flag_mode ? pack_ctas_flag : std::min(pack_ctas, kBarriers));
   const int64_t Mp = m_pad(M);
   const ncclDevComm& dc = state(c)->dev;
   if (flag_mode) {
