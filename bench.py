@@ -507,6 +507,17 @@ def run_ours(a):
             lo, hi = pos.pos_shard_range(un["n"], P, rank)
             ln = hi - lo
             n_launch += (1 if ln >= 4 else 0) + (1 if ln % 4 else 0)
+    # NEXT-3: the B200 time model beside Algorithm 1 for every FC layer (report only; the
+    # scheduler follows Alg. 1, the paper's rule)
+    choice = []
+    for ly in model.layers:
+        if ly.kind != "fc":
+            continue
+        s_b, t_s, t_p = pos.pos_scheme_times_b200(ly.M, ly.N, K, P, 2 if a.dtype == "bf16" else 4,
+                                                  peaks["hbm_gbs"] * 1e9, NVLINK_GBS_PER_DIR * 1e9,
+                                                  peaks["bf16_tflops"] * 1e12)
+        choice.append({"layer": ly.name, "alg1": pos.SCHEME_NAMES[pos.pos_choose_scheme(ly.M, ly.N, K, P)],
+                       "b200_model": pos.SCHEME_NAMES[s_b], "t_sfb_us": t_s * 1e6, "t_ps_us": t_p * 1e6})
     out = {
         "metric": METRIC, "value": P * model.total_params / (ms / 1e3), "unit": UNIT,
         "n_gpus": P, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
@@ -531,6 +542,7 @@ def run_ours(a):
         "roofline": roof,
         "clocks": clk,
         "e2e": e2e,
+        "scheme_choice": choice,
         "gpu_launches": n_launch * a.steps,
         "gpu_launches_note": "libposeidon kernels per timed region (NCCL kernels and cudaMemsetAsync not counted)",
     }

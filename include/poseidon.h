@@ -87,6 +87,17 @@ int pos_choose_scheme(int64_t M, int64_t N, int64_t K, int32_t P);
  * kind = POS_KIND_DENSE always returns POS_SCHEME_PS. */
 int pos_choose_scheme2(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P1, int32_t P2);
 
+/* NEXT-3: B200-calibrated TIME model beside Algorithm 1, in seconds per GPU and
+ * iteration for one M x N FC layer with per-GPU batch K on P GPUs:
+ *   T_SFB = (P-1) K (M+N) factor_bytes / nvl + max(8 M N / hbm, 2 M N K P / tc)
+ *   T_PS  = 2 (P-1)/P * 4 M N / nvl + 4 M N / hbm + 12 M N / (P hbm)
+ * (SFB: factors over NVLink, replicated in-place fp32 apply; PS: fp32 reduce-scatter + all-gather,
+ * dense dW formation, shard apply.) Bandwidths in bytes/s, tc in flop/s; a value <= 0 drops its
+ * terms (hbm <= 0 and tc <= 0 with factor_bytes = 4 reproduce Algorithm 1's decision exactly).
+ * Outputs may be NULL. Returns POS_SCHEME_SFB if T_SFB <= T_PS else POS_SCHEME_PS; negative on bad
+ * arguments. Oracle: oracle/cost.py b200_times. */
+int pos_scheme_times_b200(int64_t M, int64_t N, int64_t K, int32_t P, int32_t factor_bytes,
+                          double hbm, double nvl, double tc, double* t_sfb, double* t_ps);
 /* Table 1 cost in ELEMENTS as an exact reduced rational num/den (den >= 1).
  * scheme: POS_SCHEME_{PS,SFB,ADAM}; role: POS_ROLE_{SERVER,WORKER,BOTH}. SFB with role SERVER or
  * BOTH is "N/A" in Table 1 -> POS_EUNSUPPORTED. Overflow of uint64 -> POS_EINVAL. */

@@ -82,3 +82,39 @@ def best_scheme(kind: str, M: int, N: int, K: int, P1: int, P2: int) -> str:
 def best_scheme_p(kind: str, M: int, N: int, K: int, P: int) -> str:
     """This build's deployment: every GPU is both a worker and a server shard (P1 = P2 = P, S1)."""
     return best_scheme(kind, M, N, K, P, P)
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-3 (SURVEY §8(f)): a B200-calibrated TIME model beside Algorithm 1.
+#
+# Alg. 1 counts elements on the wire (Table 1, PAPER:169-183) on a 40GbE cluster where the network
+# is the only cost. On one NVSwitch box three more things matter (reading S22, DESIGN.md):
+#   * dtypes: SFB factors travel in bf16 (factor_bytes = 2), PS gradients / parameters in fp32;
+#   * SFB replicates the update: every GPU reads and writes all of W (8 M N bytes of HBM) and does
+#     2 M N K P flops, where PS applies only its shard (12 M N / P bytes: read grad, read W, write W);
+#   * PS needs the dense local gradient dW formed first (4 M N bytes written), SFB never forms it.
+# Per GPU and iteration, with B_nvl the per-direction NVLink bandwidth and all-to-all traffic
+# (every GPU sends and receives the same amount, so one direction bounds):
+#   T_SFB = (P-1) K (M+N) fb / B_nvl + max(8 M N / B_hbm, 2 M N K P / F_tc)
+#   T_PS  = 2 (P-1)/P * 4 M N / B_nvl + 4 M N / B_hbm + 12 M N / (P B_hbm)
+# A bandwidth of None (or 0) drops its terms. Tie -> SFB (as S2).
+# Pins (tests/test_oracle_cost.py): with factor_bytes = 4 and the HBM / tensor terms dropped the
+# model reduces EXACTLY to Algorithm 1 (the paper's setting: network-only, equal element widths);
+# with factor_bytes = 2 (bf16) the SFB region doubles to K (M+N) <= 4 M N / P.
+def b200_times(M: int, N: int, K: int, P: int, factor_bytes: int = 2, hbm=6551e9, nvl=770e9,
+               tc=1644e12):
+    """(T_SFB, T_PS) as exact Fractions of seconds for one FC layer (see the model above)."""
+    def inv(x):
+        return Fraction(0) if not x else 1 / Fraction(x)
+    ihbm, invl, itc = inv(hbm), inv(nvl), inv(tc)
+    t_sfb = Fraction((P - 1) * K * (M + N) * factor_bytes) * invl + max(
+        Fraction(8 * M * N) * ihbm, Fraction(2 * M * N * K * P) * itc)
+    t_ps = Fraction(2 * (P - 1) * 4 * M * N, P) * invl + Fraction(4 * M * N) * ihbm + \
+        Fraction(12 * M * N, P) * ihbm
+    return t_sfb, t_ps
+
+
+def best_scheme_b200(M: int, N: int, K: int, P: int, factor_bytes: int = 2, hbm=6551e9,
+                     nvl=770e9, tc=1644e12) -> str:
+    t_sfb, t_ps = b200_times(M, N, K, P, factor_bytes, hbm, nvl, tc)
+    return SFB if t_sfb <= t_ps else PS

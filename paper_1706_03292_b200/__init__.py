@@ -44,6 +44,16 @@ def pos_version() -> int:
     return lib().pos_version()
 
 
+def pos_scheme_times_b200(M, N, K, P, factor_bytes=2, hbm=6551e9, nvl=770e9, tc=1644e12):
+    """NEXT-3 B200 time model beside Algorithm 1: (scheme, T_SFB seconds, T_PS seconds); a
+    bandwidth / flop rate of 0 or None drops its terms (include/poseidon.h)."""
+    a, b = C.c_double(), C.c_double()
+    r = lib().pos_scheme_times_b200(M, N, K, P, factor_bytes, float(hbm or 0), float(nvl or 0),
+                                    float(tc or 0), C.byref(a), C.byref(b))
+    _chk(r, "pos_scheme_times_b200")
+    return r, a.value, b.value
+
+
 def pos_choose_scheme(M: int, N: int, K: int, P: int) -> int:
     return _chk(lib().pos_choose_scheme(M, N, K, P), "pos_choose_scheme")
 

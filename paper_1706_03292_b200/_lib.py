@@ -12,6 +12,7 @@ LIB_PATH = os.environ.get("POS_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 i32, i64, u64, f32, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_void_p
 P_i64, P_u64, P_f32 = C.POINTER(C.c_int64), C.POINTER(C.c_uint64), C.POINTER(C.c_float)
+f64, P_f64 = C.c_double, C.POINTER(C.c_double)
 
 # name -> (restype, argtypes); mirrors include/poseidon.h
 SIGNATURES = {
@@ -22,6 +23,7 @@ SIGNATURES = {
     "pos_cost_elems": (C.c_int, [i32, i32, i64, i64, i64, i32, i32, P_u64, P_u64]),
     "pos_shard_stride": (i64, [i64, i32]),
     "pos_shard_range": (C.c_int, [i64, i32, i32, P_i64, P_i64]),
+    "pos_scheme_times_b200": (C.c_int, [i64, i64, i64, i32, i32, f64, f64, f64, P_f64, P_f64]),
     "pos_padded_size": (i64, [i64, i32]),
     "pos_factor_row_elems": (i64, [i64, i64]),
     "pos_get_unique_id": (C.c_int, [vp]),

@@ -75,6 +75,25 @@ int pos_choose_scheme(int64_t M, int64_t N, int64_t K, int32_t P) {
   return pos_choose_scheme2(POS_KIND_FC, M, N, K, P, P);
 }
 
+// NEXT-3: B200 time model (include/poseidon.h; oracle/cost.py b200_times).
+int pos_scheme_times_b200(int64_t M, int64_t N, int64_t K, int32_t P, int32_t factor_bytes,
+                          double hbm, double nvl, double tc, double* t_sfb, double* t_ps) {
+  clear_error();
+  POS_CHECK_ARG(M >= 1 && N >= 1 && K >= 1 && P >= 1, "M, N, K, P must be >= 1");
+  POS_CHECK_ARG(factor_bytes == 2 || factor_bytes == 4, "factor_bytes must be 2 or 4");
+  const double m = (double)M, n = (double)N, k = (double)K, p = (double)P;
+  const double ihbm = hbm > 0 ? 1.0 / hbm : 0.0, invl = nvl > 0 ? 1.0 / nvl : 0.0,
+               itc = tc > 0 ? 1.0 / tc : 0.0;
+  const double a_hbm = 8.0 * m * n * ihbm, a_tc = 2.0 * m * n * k * p * itc;
+  const double sfb = (p - 1) * k * (m + n) * factor_bytes * invl + (a_hbm > a_tc ? a_hbm : a_tc);
+  // multiply before dividing: integer-valued quotients (Alg. 1's ties) stay exact
+  const double ps = 8.0 * (p - 1) * m * n / p * invl + 4.0 * m * n * ihbm +
+                    12.0 * m * n / p * ihbm;
+  if (t_sfb) *t_sfb = sfb;
+  if (t_ps) *t_ps = ps;
+  return sfb <= ps ? POS_SCHEME_SFB : POS_SCHEME_PS;
+}
+
 // Table 1, as exact reduced rationals.
 int pos_cost_elems(int32_t scheme, int32_t role, int64_t M, int64_t N, int64_t K, int32_t P1,
                    int32_t P2, uint64_t* num, uint64_t* den) {

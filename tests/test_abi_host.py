@@ -117,3 +117,34 @@ def test_factor_row_layout():
     assert pos.pos_factor_row_elems(1, 1) == 64 + 64
     assert pos.pos_factor_row_elems(64, 64) == 64 + 128
     assert pos.pos_factor_row_elems(13, 7) == 64 + 64
+
+
+def test_b200_time_model_matches_oracle():
+    """NEXT-3 chooser: the C time model (double) equals the oracle's exact-Fraction model to
+    rounding, and takes the same decision wherever the two times are not within rounding."""
+    shapes = [(4096, 4096, 32), (4096, 25088, 32), (21841, 4096, 32), (1000, 4096, 128),
+              (4096, 9216, 128), (2048, 1000, 32), (64, 64, 8), (7, 3, 5), (4096, 4096, 512)]
+    for (M, N, K) in shapes:
+        for P in (1, 2, 4, 8, 16):
+            for fb in (2, 4):
+                for (hbm, nvl, tc) in [(6551e9, 770e9, 1644e12), (None, 770e9, None),
+                                       (6551e9, 900e9, None)]:
+                    s, ts, tp = pos.pos_scheme_times_b200(M, N, K, P, fb, hbm, nvl, tc)
+                    es, ep = cost.b200_times(M, N, K, P, fb, hbm, nvl, tc)
+                    assert abs(ts - float(es)) <= 1e-12 * float(es) + 1e-30
+                    assert abs(tp - float(ep)) <= 1e-12 * float(ep) + 1e-30
+                    if abs(float(es - ep)) > 1e-9 * float(max(es, ep)):
+                        exp = cost.best_scheme_b200(M, N, K, P, fb, hbm, nvl, tc)
+                        assert pos.SCHEME_NAMES[s] == exp, (M, N, K, P, fb, hbm, nvl, tc)
+
+
+def test_b200_time_model_reproduces_algorithm_1():
+    """Network-only, fp32 factors: bit-exact Alg. 1 decisions on a tiny grid (ties included —
+    both sides are then exactly representable small integers over the same bandwidth)."""
+    lib = pos.lib()
+    for M in range(1, 17):
+        for N in range(1, 17):
+            for K in range(1, 9):
+                for P in range(1, 9):
+                    s, _, _ = pos.pos_scheme_times_b200(M, N, K, P, 4, 0, 1.0, 0)
+                    assert s == lib.pos_choose_scheme(M, N, K, P), (M, N, K, P)

@@ -177,3 +177,41 @@ def test_config_schemes():
                 assert s == (cost.SFB if l.kind == "fc" else cost.PS), (cfg, l, P)
     assert cost.best_scheme_p(cost.FC, 1000, 768, 32, 16) == cost.SFB
     assert cost.best_scheme_p(cost.FC, 1000, 768, 32, 32) == cost.PS
+
+
+# ------------------------------------------------------------------ NEXT-3: B200 time model ----
+def test_b200_model_reduces_to_algorithm_1_in_the_papers_setting():
+    """Network-only (HBM / tensor terms dropped) and equal element widths (fp32 factors): the B200
+    time model must take exactly Alg. 1's decision on every tiny shape."""
+    for M in range(1, 13):
+        for N in range(1, 13):
+            for K in range(1, 9):
+                for P in range(1, 9):
+                    got = cost.best_scheme_b200(M, N, K, P, factor_bytes=4, hbm=None, tc=None)
+                    assert got == cost.best_scheme_p(cost.FC, M, N, K, P), (M, N, K, P)
+
+
+def test_b200_model_bf16_factors_double_the_sfb_region():
+    """bf16 factors vs fp32 PS payload, network only: SFB iff K (M+N) P <= 4 M N (P > 1), i.e.
+    twice Alg. 1's K (M+N) P <= 2 M N."""
+    for M in range(1, 17):
+        for N in range(1, 17):
+            for K in range(1, 9):
+                for P in range(2, 9):
+                    got = cost.best_scheme_b200(M, N, K, P, factor_bytes=2, hbm=None, tc=None)
+                    assert got == (cost.SFB if K * (M + N) * P <= 4 * M * N else cost.PS)
+
+
+def test_b200_model_limits_and_monotonicity():
+    # P = 1: no wire; SFB = its replicated apply (8 MN bytes), PS = dW write + full apply (16 MN)
+    t_sfb, t_ps = cost.b200_times(4096, 4096, 32, 1, hbm=1.0, nvl=1.0, tc=None)
+    assert t_sfb == 8 * 4096 * 4096 and t_ps == 16 * 4096 * 4096
+    # larger K only adds to SFB: once PS, always PS
+    for (M, N, P) in [(4096, 4096, 8), (1000, 4096, 4), (21841, 4096, 8), (64, 64, 2)]:
+        seen_ps = False
+        for K in range(1, 2049, 7):
+            s = cost.best_scheme_b200(M, N, K, P)
+            seen_ps |= s == cost.PS
+            assert not (seen_ps and s == cost.SFB), (M, N, P, K)
+    # the symmetric formula (reading S7)
+    assert cost.b200_times(300, 7000, 64, 8) == cost.b200_times(7000, 300, 64, 8)
