@@ -133,6 +133,31 @@ def _worker(rank, world, port, outdir):
         check("sfb_stat_W", err(g3, Wr3) <= 2e-3)
         check("sfb_stat_dW", err(g3 - W30, Wr3 - W30) <= 2e-3)
         res["digests"]["sfb_stat"] = _digest(W3)
+        # ---- (f) scheduler SFB: tf32 (flag-mode gather, double buffer), fp32 (barrier-mode
+        #          multicast + SIMT reconstruction) and a CTA-pair layer (K*P = 1024); 3 iterations
+        def run_dtype(dt, in_dt, Kx, Mx, Nx, iters=3):
+            sch = pos.Scheduler(ctx, 1)
+            U, V = zip(*(si.exact_factors(si.rng(49, Kx, p), Kx, Mx, Nx) for p in range(P)))
+            w0_ = si.exact_weights(si.rng(49, 1), Mx, Nx)
+            b0_ = si.exact_weights(si.rng(49, 2), Mx)
+            Wx, Bx = to_dev(w0_), to_dev(b0_)
+            assert sch.add_fc(0, Mx, Nx, Kx, Wx, Bx, None, dt, in_dt) == pos.POS_SCHEME_SFB
+            st = "bf16" if in_dt == pos.POS_IN_BF16 else "f32"
+            u, v = to_dev(U[rank], st), to_dev(V[rank], st)
+            for _ in range(iters):
+                sch.begin(a)
+                sch.factors_ready(0, u, v, torch.cuda.current_stream())
+                sch.end(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            wr, br_ = w0_, b0_
+            for _ in range(iters):
+                wr, br_ = sync.sfb_update(wr, br_, U, V, a)
+            ok = np.array_equal(to_host(Wx), wr) and np.array_equal(to_host(Bx), br_)
+            sch.close()
+            return ok
+        check("sched_tf32_flags_3iter", run_dtype("tf32", pos.POS_IN_F32, 16, 1000, 1028))
+        check("sched_f32_barrier_3iter", run_dtype("f32", pos.POS_IN_F32, 16, 300, 132))
+        check("sched_pair_3iter", run_dtype("bf16", pos.POS_IN_BF16, 1024 // P, 2000, 4100))
         # ---- (e) WFBP scheduler: FC (SFB) + bucket + dense; WFBP == sequential, both == oracle --
         def run_sched(sequential, graph, symm_dense=False, iters=1):
             alloc = (lambda k: ctx.sym_empty(k)) if symm_dense else (lambda k: torch.zeros(k, device=dev))
