@@ -128,6 +128,60 @@ ps_nvls_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, s
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // every replica's W is complete
 }
 
+// P = 2 variant of the fused PS step with plain peer loads / stores over NVLink (LSA pointers):
+// per GPU and direction it moves n/2 + n/2 fp32 words where the NVLS path moves ~1.5 n (the switch
+// reads every copy, including the local one, and writes every replica). Sum in rank order.
+__global__ void __launch_bounds__(kPsThreads)
+ps_p2p2_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, size_t off_w,
+               int64_t lo, int64_t hi, float alpha) {
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
+  bar.sync(ncclCoopCta(), kEntryOrder);     // both gradients are in place (see ps_nvls_kernel)
+  const float* g0 = static_cast<const float*>(ncclGetLsaPointer(wg, off_g, 0));
+  const float* g1 = static_cast<const float*>(ncclGetLsaPointer(wg, off_g, 1));
+  float* w0 = static_cast<float*>(ncclGetLsaPointer(ww, off_w, 0));
+  float* w1 = static_cast<float*>(ncclGetLsaPointer(ww, off_w, 1));
+  const float* wl = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
+  const int64_t v0 = lo / 4, v1 = hi / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kPsUnroll - 1) * stride < v1; i += kPsUnroll * stride) {
+    float4 a[kPsUnroll], b[kPsUnroll], w[kPsUnroll];
+#pragma unroll
+    for (int u = 0; u < kPsUnroll; ++u) {
+      a[u] = *reinterpret_cast<const float4*>(g0 + 4 * (i + u * stride));
+      b[u] = *reinterpret_cast<const float4*>(g1 + 4 * (i + u * stride));
+      w[u] = *reinterpret_cast<const float4*>(wl + 4 * (i + u * stride));
+    }
+#pragma unroll
+    for (int u = 0; u < kPsUnroll; ++u) {
+      w[u].x = fmaf(alpha, a[u].x + b[u].x, w[u].x);
+      w[u].y = fmaf(alpha, a[u].y + b[u].y, w[u].y);
+      w[u].z = fmaf(alpha, a[u].z + b[u].z, w[u].z);
+      w[u].w = fmaf(alpha, a[u].w + b[u].w, w[u].w);
+      *reinterpret_cast<float4*>(w0 + 4 * (i + u * stride)) = w[u];
+      *reinterpret_cast<float4*>(w1 + 4 * (i + u * stride)) = w[u];
+    }
+  }
+  for (; i < v1; i += stride) {
+    const float4 a = *reinterpret_cast<const float4*>(g0 + 4 * i);
+    const float4 b = *reinterpret_cast<const float4*>(g1 + 4 * i);
+    float4 w = *reinterpret_cast<const float4*>(wl + 4 * i);
+    w.x = fmaf(alpha, a.x + b.x, w.x);
+    w.y = fmaf(alpha, a.y + b.y, w.y);
+    w.z = fmaf(alpha, a.z + b.z, w.z);
+    w.w = fmaf(alpha, a.w + b.w, w.w);
+    *reinterpret_cast<float4*>(w0 + 4 * i) = w;
+    *reinterpret_cast<float4*>(w1 + 4 * i) = w;
+  }
+  if (blockIdx.x == 0)   // scalar tail of the shard
+    for (int64_t j = v1 * 4 + threadIdx.x; j < hi; j += blockDim.x) {
+      const float w = fmaf(alpha, g0[j] + g1[j], wl[j]);
+      w0[j] = w;
+      w1[j] = w;
+    }
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // both replicas of W are complete
+}
+
 __device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ float ld_in(const float* p) { return *p; }
 
@@ -326,7 +380,18 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
     return v < 1 ? 1 : (v > kBarriers ? kBarriers : v);
   }();
   const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, ps_ctas);
-  ps_nvls_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
+  // P = 2 option (POS_PS_P2P=1): plain peer loads / stores move less over NVLink than the switch
+  // path — 10-20% faster alone (80 MB: 196 vs 218 us), but its NVLink traffic through the SMs'
+  // load/store path slows a concurrent reconstruction far more (VGG19-22K step 0.55 vs 0.45 ms);
+  // only the PS-only Inception-V3 step gains (-8%), so the NVLS kernel stays the default
+  static const bool p2p2 = [] {
+    const char* e = getenv("POS_PS_P2P");
+    return e && e[0] == '1';
+  }();
+  if (P == 2 && p2p2)
+    ps_p2p2_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
+  else
+    ps_nvls_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_nvls_kernel launch");
   if (ev_a1) POS_CUDA_TRY(record_timing_event(ev_a1, s));
