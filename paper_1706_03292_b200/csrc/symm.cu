@@ -373,12 +373,16 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   int64_t lo = 0, hi = 0;
   pos_shard_range(n, P, c->rank, &lo, &hi);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
-  // NVLS loads have microsecond latency: keep ~2 MB of reductions in flight per GPU
-  static const int ps_ctas = [] {
+  // NVLS loads have microsecond latency. Measured (VGG19-22K / VGG19 steps, next to the
+  // reconstructions): P = 2 — each rank reduces half of every unit — wants 64 CTAs (0.45 -> 0.41 ms;
+  // 16: 0.52, 128: 0.47); P = 4 is best at 24-48 (64 hung once at P = 4: NVLS CTAs spinning in
+  // their barrier can starve the reconstructions and packs of SM slots), hence 32 for P >= 3.
+  static const int ps_ctas_env = [] {
     const char* e = getenv("POS_NVLS_CTAS");
-    const int v = (e && *e) ? atoi(e) : 32;
-    return v < 1 ? 1 : (v > kBarriers ? kBarriers : v);
+    return (e && *e) ? atoi(e) : 0;
   }();
+  int ps_ctas = ps_ctas_env > 0 ? ps_ctas_env : (P == 2 ? 64 : 32);
+  if (ps_ctas > kBarriers) ps_ctas = kBarriers;
   const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, ps_ctas);
   // P = 2 option (POS_PS_P2P=1): plain peer loads / stores move less over NVLink than the switch
   // path — 10-20% faster alone (80 MB: 196 vs 218 us), but its NVLink traffic through the SMs'
