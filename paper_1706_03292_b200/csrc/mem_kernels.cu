@@ -7,6 +7,8 @@
 // on the side that dominates the traffic.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.h"
 
 namespace pos {
@@ -162,7 +164,12 @@ __global__ void sim_ps_reduce_apply_kernel(GradPtrs gp, int P, float* __restrict
 
 int grid_for(int64_t work_items, int threads) {
   int64_t blocks = (work_items + threads - 1) / threads;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  static const int64_t mult = [] {   // CTAs per SM cap of the streaming kernels
+    const char* e = getenv("POS_STREAM_CTAS_PER_SM");
+    const int v = (e && *e) ? atoi(e) : 8;
+    return (int64_t)(v < 1 ? 1 : v);
+  }();
+  const int64_t cap = (int64_t)num_sms() * mult;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return (int)blocks;
