@@ -335,3 +335,47 @@ def test_sched_dynamic_tiles_bitwise_equal_static_and_repeatable(pair, monkeypat
         sch.close()
         ctx.close()
     assert np.array_equal(res[0], res[1])
+
+
+def test_sched_wait_layer_raw_gate_per_layer():
+    """pos_sched_wait_layer (the per-layer RAW gate for the next forward): a consumer
+    stream that waits for ONE layer reads that layer's updated W while another layer's sync is
+    still held back behind a slow producer (device sleep before its trigger)."""
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, 2)
+    a = si.EXACT_ALPHA
+    dims = [(1000, 4100, 16), (4096, 4096, 16)]
+    host, dev = [], []
+    for l, (M, N, K) in enumerate(dims):
+        g = si.rng(70, l)
+        u, v = si.exact_factors(g, K, M, N)
+        W, b = si.exact_weights(g, M, N), si.exact_weights(g, M)
+        host.append((W, b, u, v))
+        Wd, bd = to_dev(W), to_dev(b)
+        assert sch.add_fc(l, M, N, K, Wd, bd, None, "bf16", pos.POS_IN_BF16) == pos.POS_SCHEME_SFB
+        dev.append((Wd, bd, to_dev(u, "bf16"), to_dev(v, "bf16")))
+    producer, consumer = torch.cuda.Stream(), torch.cuda.Stream()
+    producer.wait_stream(torch.cuda.current_stream())
+    consumer.wait_stream(torch.cuda.current_stream())
+    sch.begin(a)
+    with torch.cuda.stream(producer):
+        sch.factors_ready(1, dev[1][2], dev[1][3], producer)     # b^2 done: layer 1 issued now
+        torch.cuda._sleep(200_000_000)                          # a slow b^1 (~0.1 s)
+        sch.factors_ready(0, dev[0][2], dev[0][3], producer)
+    sch.wait_layer(1, consumer)                                 # f^2 of the next iteration
+    done1 = torch.cuda.Event()
+    with torch.cuda.stream(consumer):
+        snap = dev[1][0].clone()                                # reads W^2 after its sync only
+        done1.record(consumer)
+    done1.synchronize()
+    still_running = not producer.query()                        # layer 0 still held back
+    sch.end(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    W1, b1 = sync.sfb_update(host[1][0], host[1][1], [host[1][2]], [host[1][3]], a)
+    W0, b0 = sync.sfb_update(host[0][0], host[0][1], [host[0][2]], [host[0][3]], a)
+    assert np.array_equal(to_host(snap), W1)
+    assert np.array_equal(to_host(dev[1][0]), W1) and np.array_equal(to_host(dev[0][0]), W0)
+    assert np.array_equal(to_host(dev[0][1]), b0)
+    assert still_running, "the gate waited for the whole iteration, not for layer 1 only"
+    sch.close()
+    ctx.close()
