@@ -404,7 +404,7 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
       const char* e = getenv("POS_GATHER_FLAGS");
       return e && e[0] == '0';
     }();
-    const bool fm = !flags_off && dtype != POS_DT_F32 && (N % 4) == 0;
+    const bool fm = !flags_off && dtype != POS_DT_F32 && (N % 4) == 0 && aligned16(W);
     const size_t al = (bytes + 255) & ~size_t(255);
     const size_t total = fm ? 2 * al + 256 : bytes;
     if (pos_mem_alloc(c, (int64_t)total, &u.gbuf) == POS_OK) {
