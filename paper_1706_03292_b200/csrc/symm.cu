@@ -376,12 +376,13 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   // NVLS loads have microsecond latency. Measured (VGG19-22K / VGG19 steps, next to the
   // reconstructions): P = 2 — each rank reduces half of every unit — wants 64 CTAs (0.45 -> 0.41 ms;
   // 16: 0.52, 128: 0.47); P = 4 is best at 24-48 (64 hung once at P = 4: NVLS CTAs spinning in
-  // their barrier can starve the reconstructions and packs of SM slots), hence 32 for P >= 3.
+  // their barrier can starve the reconstructions and packs of SM slots). Rule: 128 / P CTAs (the
+  // same shard bytes per CTA at every P), at least 16 — P = 8 (not measurable here) gets 16.
   static const int ps_ctas_env = [] {
     const char* e = getenv("POS_NVLS_CTAS");
     return (e && *e) ? atoi(e) : 0;
   }();
-  int ps_ctas = ps_ctas_env > 0 ? ps_ctas_env : (P == 2 ? 64 : 32);
+  int ps_ctas = ps_ctas_env > 0 ? ps_ctas_env : std::max(16, 128 / P);
   if (ps_ctas > kBarriers) ps_ctas = kBarriers;
   const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, ps_ctas);
   // P = 2 option (POS_PS_P2P=1): plain peer loads / stores move less over NVLink than the switch
