@@ -153,6 +153,112 @@ def roofline_times(rows, peaks, P):
     return max(t_nvl, t_k), t_seq, t_nvl, t_k
 
 
+# ------------------------------------------------------------------------ the timed step --
+def device_fill(gen, dtype):
+    """Timing-run values, generated on the device: u = 2^-5 N(0,1), v = ReLU(N(0,1)),
+    W ~ U(+-1/sqrt(N)), dense W ~ U(+-0.05), dense grads 2^-5 N(0,1)."""
+    import torch
+    fdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+
+    def fill(kind, layer, t, role):
+        n = t.numel()
+        if role == "W" and kind == "fc":
+            t.copy_((torch.rand(t.shape, device=t.device, generator=gen) * 2 - 1) / math.sqrt(t.shape[1]))
+        elif role == "b":
+            t.zero_()
+        elif role == "u":
+            t.copy_((torch.randn(t.shape, device=t.device, generator=gen) * 2 ** -5).to(fdt))
+        elif role == "v":
+            t.copy_(torch.relu(torch.randn(t.shape, device=t.device, generator=gen)).to(fdt))
+        elif role == "W":
+            t.copy_((torch.rand(n, device=t.device, generator=gen) * 2 - 1) * 0.05)
+        else:   # dense gradient
+            t.copy_(torch.randn(n, device=t.device, generator=gen) * 2 ** -5)
+    return fill
+
+
+def register_units(pos, ctx, sch, model, units, K, dtype, fill, symm=True):
+    """Register every synchronisation unit of the plan with the scheduler (SFB FC layers; dense
+    buckets in symmetric memory when P > 1, so the fused NVLS kernels run), allocate its buffers and
+    fill them with fill(kind, layer, tensor, role). Returns per-layer buffer records."""
+    import torch
+    P = ctx.world
+    dev = torch.device("cuda", torch.cuda.current_device())
+    in_dt = pos.POS_IN_BF16 if dtype == "bf16" else pos.POS_IN_F32
+    fdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    bufs = [None] * len(model.layers)
+    for un in units:
+        if un["kind"] == "fc":
+            l = un["layers"][0]
+            ly = model.layers[l]
+            M, N = ly.M, ly.N
+            W = torch.empty(M, N, device=dev)
+            fill("fc", l, W, "W")
+            b = None
+            if ly.bias:
+                b = torch.empty(M, device=dev)
+                fill("fc", l, b, "b")
+            u = torch.empty(K, M, device=dev, dtype=fdt)
+            v = torch.empty(K, N, device=dev, dtype=fdt)
+            fill("fc", l, u, "u")
+            fill("fc", l, v, "v")
+            s = sch.add_fc(l, M, N, K, W, b, None, dtype=dtype, in_dtype=in_dt)
+            assert s == pos.POS_SCHEME_SFB, (ly, s)   # Alg. 1 at these configs (SURVEY §8(a) A0)
+            bufs[l] = {"kind": "fc", "W": W, "b": b, "u": u, "v": v}
+        else:
+            n = un["n"]
+            Pn = pos.pos_padded_size(n, P)
+            sy = P > 1 and symm       # the fused NVLS PS kernel needs symmetric W and grad
+            W = ctx.sym_empty(Pn) if sy else torch.zeros(Pn, device=dev)
+            g = ctx.sym_empty(Pn) if sy else torch.zeros(Pn, device=dev)
+            off = 0
+            for l, nl in zip(un["layers"], un["sizes"]):
+                fill("dense", l, W[off:off + nl], "W")
+                fill("dense", l, g[off:off + nl], "g")
+                off += nl
+            g0 = g.clone()
+            sch.add_dense_bucket(un["layers"][0], un["sizes"], W, g)
+            off = 0
+            for l, nl in zip(un["layers"], un["sizes"]):
+                bufs[l] = {"kind": "dense", "W": W[off:off + nl], "g": g[off:off + nl],
+                           "g0": g0[off:off + nl], "n": nl, "Wflat": W, "gflat": g}
+                off += nl
+    return bufs
+
+
+def make_step(sch, bufs, alpha):
+    """One full-model synchronisation (Algorithm 2): begin, every layer triggered in backward order
+    b^L .. b^1, end on the caller's stream."""
+    L = len(bufs)
+
+    def step(stream):
+        sch.begin(alpha)
+        for l in range(L - 1, -1, -1):
+            bb = bufs[l]
+            if bb["kind"] == "fc":
+                sch.factors_ready(l, bb["u"], bb["v"], stream)
+            else:
+                sch.grad_ready(l, stream)
+        sch.end(stream)
+    return step
+
+
+def capture_ring(fn, main, n=4):
+    """CUDA graphs of one step each: replaying them round-robin keeps n timing-event slots of the
+    scheduler live (slot = iteration mod 4), so per-kernel timings stay measurable."""
+    import torch
+    gs = []
+    cs = torch.cuda.Stream()
+    cs.wait_stream(main)
+    for _ in range(n):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+            fn(torch.cuda.current_stream())
+        gs.append(g)
+    main.wait_stream(cs)
+    return gs
+
+
 # ------------------------------------------------------------------------------ clocks ------
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -246,52 +352,16 @@ def run_ours(a):
     model = si.load_model(model_name)
     L = len(model.layers)
     alpha = -0.01 / P
-    in_dt = pos.POS_IN_BF16 if a.dtype == "bf16" else pos.POS_IN_F32
-    fdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * 1 + rank)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
     sch = pos.Scheduler(ctx, L, timing=("apply" if not a.layers else True), sequential=a.sequential,
                         symm=not a.no_symm, ps_after_sfb=a.ps_after_sfb, static_tiles=a.static_tiles)
-    bufs = [None] * L
-    for un in units:
-        if un["kind"] == "fc":
-            l = un["layers"][0]
-            ly = model.layers[l]
-            M, N = ly.M, ly.N
-            W = (torch.rand(M, N, device=dev, generator=gen) * 2 - 1) / math.sqrt(N)
-            b = torch.zeros(M, device=dev) if ly.bias else None
-            u = (torch.randn(K, M, device=dev, generator=gen) * 2 ** -5).to(fdt)
-            v = torch.relu(torch.randn(K, N, device=dev, generator=gen)).to(fdt)
-            s = sch.add_fc(l, M, N, K, W, b, None, dtype=a.dtype, in_dtype=in_dt)
-            assert s == pos.POS_SCHEME_SFB, (ly, s)   # Alg. 1 at these configs
-            bufs[l] = {"kind": "fc", "W": W, "b": b, "u": u, "v": v}
-        else:
-            n = un["n"]
-            Pn = pos.pos_padded_size(n, P)
-            symm = P > 1 and not a.no_symm       # NVLS fused PS kernel needs symmetric W and grad
-            W = ctx.sym_empty(Pn) if symm else torch.zeros(Pn, device=dev)
-            W[:n] = (torch.rand(n, device=dev, generator=gen) * 2 - 1) * 0.05
-            g = ctx.sym_empty(Pn) if symm else torch.zeros(Pn, device=dev)
-            g[:n] = torch.randn(n, device=dev, generator=gen) * 2 ** -5
-            g0 = g.clone()
-            sch.add_dense_bucket(un["layers"][0], un["sizes"], W, g)
-            off = 0
-            for l, nl in zip(un["layers"], un["sizes"]):
-                bufs[l] = {"kind": "dense", "W": W[off:off + nl], "g": g[off:off + nl], "g0": g0[off:off + nl], "n": nl}
-                off += nl
+    bufs = register_units(pos, ctx, sch, model, units, K, a.dtype, device_fill(gen, a.dtype),
+                          symm=not a.no_symm)
     main = torch.cuda.current_stream()
-
-    def step(stream):
-        sch.begin(alpha)
-        for l in range(L - 1, -1, -1):      # backward order: b^L .. b^1
-            bb = bufs[l]
-            if bb["kind"] == "fc":
-                sch.factors_ready(l, bb["u"], bb["v"], stream)
-            else:
-                sch.grad_ready(l, stream)
-        sch.end(stream)
+    step = make_step(sch, bufs, alpha)
 
     def barrier():
         if world > 1:
@@ -301,20 +371,6 @@ def run_ours(a):
         for bb in bufs:
             if bb["kind"] == "dense":
                 bb["g"].copy_(bb["g0"])
-
-    def capture_ring(fn, n=4):
-        """CUDA graphs of one step each: replaying them round-robin keeps n timing-event slots of
-        the scheduler live (slot = iteration mod 4), so per-kernel timings stay measurable."""
-        gs = []
-        cs = torch.cuda.Stream()
-        cs.wait_stream(main)
-        for _ in range(n):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
-                fn(torch.cuda.current_stream())
-            gs.append(g)
-        main.wait_stream(cs)
-        return gs
 
     # ---- warmup (untimed, eager: NCCL connections, launch plans) ----
     _log(f"{len(units)} units registered; warmup")
@@ -326,7 +382,7 @@ def run_ours(a):
     if a.eager:
         run = lambda i: step(main)
     else:
-        graphs = capture_ring(step)
+        graphs = capture_ring(step, main)
         _log("captured")
         run = lambda i: graphs[i % len(graphs)].replay()
         for i in range(len(graphs)):
@@ -426,7 +482,7 @@ def run_ours(a):
         if a.eager:
             run_e2e = lambda i: e2e_step(main)
         else:
-            g_e2e = capture_ring(e2e_step)
+            g_e2e = capture_ring(e2e_step, main)
             run_e2e = lambda i: g_e2e[i % len(g_e2e)].replay()
         for i in range(4):
             run_e2e(i)

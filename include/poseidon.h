@@ -38,6 +38,7 @@ extern "C" {
 
 typedef struct pos_ctx pos_ctx;
 typedef struct pos_sched pos_sched;
+typedef struct pos_loop_fc pos_loop_fc;
 
 /* Communication schemes (§3.2, Table 1). ADAM only for pos_cost_elems. */
 enum { POS_SCHEME_PS = 0, POS_SCHEME_SFB = 1, POS_SCHEME_ADAM = 2 };
@@ -55,8 +56,17 @@ enum { POS_IN_BF16 = 0, POS_IN_F32 = 1 };
 /* Error codes. */
 enum {
   POS_OK = 0, POS_EINVAL = -1, POS_ESTATE = -2, POS_ECUDA = -3, POS_ENCCL = -4,
-  POS_ENOMEM = -5, POS_EUNSUPPORTED = -6
+  POS_ENOMEM = -5, POS_EUNSUPPORTED = -6,
+  POS_ETIMEOUT = -7   /* a cross-GPU wait exceeded the context's timeout (sticky) */
 };
+/* Summation order of the PS reduce (pos_set_reduce_order). SWITCH: multimem.ld_reduce, the NVSwitch
+ * adds the P gradients (its order); RANK_ORDER: every rank loads the P gradients of its shard from
+ * its peers and adds them in rank order 0..P-1 — bitwise reproducible run to run. */
+enum { POS_REDUCE_SWITCH = 0, POS_REDUCE_RANK_ORDER = 1 };
+/* Fault injection (pos_inject_fault; tests of the watchdog):
+ *   SKIP_PS  : the given rank does not launch its fused PS kernels (its peers' barriers time out);
+ *   SKIP_PACK: loopback only — the given simulated rank does not pack (the flag waits time out). */
+enum { POS_FAULT_NONE = 0, POS_FAULT_SKIP_PS = 1, POS_FAULT_SKIP_PACK = 2 };
 /* pos_sched_create flags: TIMING = per-unit pack / collective / apply stage events;
  * TIMING_APPLY = only the apply stage (reconstruct-and-apply, shard apply) is bracketed, which
  * adds the fewest graph nodes; SEQUENTIAL = WFBP off (sync after the whole backward). */
@@ -67,7 +77,7 @@ enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2, POS_SCHED_TIMING_APPLY = 
        POS_SCHED_STATIC_TILES = 32 /* reconstruction tiles in static round-robin order instead of
                                       the dynamic (atomic-counter) tile scheduler */ };
 
-/* ABI version (major * 100 + minor). */
+/* ABI version (major * 100 + minor): 200 = split factors_ready / weights_free trigger events, watchdog, loopback. */
 int pos_version(void);
 /* Message of the last < 0 return on this host thread ("" if none). Never NULL. */
 const char* pos_last_error(void);
@@ -137,8 +147,19 @@ int pos_init_local(int32_t P_sim, pos_ctx** out);
 int pos_finalize(pos_ctx* ctx);
 int pos_world(const pos_ctx* ctx);
 int pos_rank(const pos_ctx* ctx);
-/* Sticky asynchronous CUDA/NCCL error (POS_OK if none). */
+/* Sticky asynchronous CUDA/NCCL/watchdog error (POS_OK if none). Does not synchronise: a watchdog
+ * expiry is read from a host-mapped error word the kernels write (POS_ETIMEOUT, with the waiting
+ * site in pos_last_error()). */
 int pos_get_async_error(pos_ctx* ctx);
+/* Watchdog budget for every cross-GPU wait inside the library's kernels (entry / exit barriers of
+ * the fused PS and gather kernels, gather ready flags): after `ms` milliseconds of spinning the
+ * kernel records POS_ETIMEOUT and returns instead of hanging (results of that iteration are
+ * undefined; the context is poisoned). 0 = unbounded. Default: env POS_TIMEOUT_MS, else 20000. */
+int pos_set_timeout_ms(pos_ctx* ctx, int64_t ms);
+/* PS reduce order (POS_REDUCE_*); every rank must set the same. Default POS_REDUCE_SWITCH. */
+int pos_set_reduce_order(pos_ctx* ctx, int32_t order);
+/* Fault injection for tests (POS_FAULT_*); rank = the rank that misbehaves. */
+int pos_inject_fault(pos_ctx* ctx, int32_t kind, int32_t rank);
 /* Symmetric (NVLink-SHARP multicast) memory, NEXT-1 of SURVEY §8(f). COLLECTIVE: every rank calls
  * with the same size in the same order. The buffer is an NCCL symmetric window on an NVLS
  * multicast object, zero-filled. When a PS layer's W and grad both live in such buffers, its
@@ -220,19 +241,50 @@ int pos_sim_sync_layer_sfb(pos_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_
 int pos_sim_sync_layer_ps(pos_ctx* ctx, int64_t n, const float* const* grads, float* W,
                           float alpha, void* stream);
 
+/* LOOPBACK (single GPU, P = the context's simulated ranks, pos_init_local(P), P <= 16): the SAME
+ * kernels as the P > 1 symmetric-memory path, with every cross-GPU address taken from a table of
+ * P local replicas and the ranks executed one after the other in stream order (so no barrier is
+ * needed). Lets one GPU check the P > 1 kernel bodies (shard reduce -> apply -> broadcast; pack ->
+ * slot -> flag publication -> flag wait -> double-buffered reconstruction) against the oracle.
+ *
+ * PS: for r = 0..P-1, rank r reduces grads[0..P-1] on its shard in rank order, applies
+ * W[r][shard] += alpha * sum, and stores the result into the shard of every W[p]. grads[p], W[p]:
+ * device fp32, 16-byte aligned, >= pos_padded_size(n, P) elements. */
+int pos_loop_sync_layer_ps(pos_ctx* ctx, int64_t n, float* const* grads, float* const* W,
+                           float alpha, void* stream);
+/* SFB: a loopback FC layer with P replicas W[p] (M x N fp32 row-major, 16-byte
+ * aligned) and optional b[p] (M). Tensor-core dtypes with N % 4 == 0 use the flag-mode protocol
+ * (double-buffered gather buffers per replica, ready flags, device-side buffer selection); other
+ * layers the barrier-mode layout. The library owns P gather buffers. */
+int pos_loop_fc_create(pos_ctx* ctx, int64_t M, int64_t N, int64_t K, int32_t dtype,
+                       float* const* W, float* const* b, pos_loop_fc** out);
+/* One iteration: every rank r packs (u[r], v[r]) (K x M / K x N, in_dtype) into its slot of every
+ * replica's gather buffer; then every replica waits for the P ready flags and reconstructs
+ * W[p] += alpha * U^T V, b[p] += alpha * colsum(U). */
+int pos_loop_fc_sync(pos_loop_fc* lf, int32_t in_dtype, const void* const* u, const void* const* v,
+                     float alpha, void* stream);
+int pos_loop_fc_destroy(pos_loop_fc* lf);
+
 /* ======================================================================================
  * WFBP scheduler (§3.1, Algorithm 2, vector C PAPER:273-275).
  * One record per layer ("syncer"). Per iteration:
  *   pos_sched_begin  -> C := 0
- *   for l = L..1 as backward produces them:
- *     FC  : pos_sched_factors_ready(l, u, v, stream)   (after b^l read W: u, v ready, W free)
- *     DENSE: pos_sched_grad_ready(l, stream)           (after dW of layer l is in grad)
+ *   for l = L..1 as backward produces them (Alg. 2 L6-L7):
+ *     FC   : pos_sched_factors_ready(l, K, u, v, factors_ready, weights_free)
+ *     DENSE: pos_sched_grad_ready(l, grad_ready)
  *   pos_sched_end(consumer)   -> consumer stream waits until all of C is 1 (Alg. 2 L8)
- * Each trigger records an event on the caller's `stream` and enqueues the layer's sync on the
- * library's streams (one comm stream, a pool of apply streams), so s^l overlaps b^i, i < l.
+ * A trigger takes CUDA events the caller recorded on its backward stream and enqueues the layer's
+ * sync on the library's streams (one comm stream, a pool of apply streams) behind them, so s^l
+ * overlaps b^i, i < l. An event must not be re-recorded until its unit is issued (at
+ * the trigger of the unit's last layer; at pos_sched_end with POS_SCHED_SEQUENTIAL).
  * Layer indices are 0-based in forward order. Buffers passed at add time must outlive the
  * scheduler. Calls return POS_ESTATE on misuse (trigger twice, end before all triggered,
  * add after begin).
+ * Cross-iteration contract (WAR on the library's gather buffers): the triggers of iteration s+1
+ * must be stream-ordered after pos_sched_end of iteration s on its consumer stream (or after
+ * pos_sched_wait_layer of the same layer) — e.g. the next backward runs on the consumer stream.
+ * The flag-mode gather (P > 1, tensor-core dtypes) double-buffers and tolerates one iteration of
+ * slack beyond that; the barrier-mode and NCCL gathers do not.
  * ====================================================================================== */
 int pos_sched_create(pos_ctx* ctx, int32_t n_layers, int32_t flags, pos_sched** out);
 /* FC layer. force_scheme = -1 applies Algorithm 1; else POS_SCHEME_SFB / POS_SCHEME_PS.
@@ -252,12 +304,33 @@ int pos_sched_add_dense_bucket(pos_sched* s, int32_t l_first, int32_t count, con
 /* Index of the synchronisation unit (layer or bucket) that layer l belongs to. */
 int pos_sched_unit_of(pos_sched* s, int32_t l);
 int pos_sched_begin(pos_sched* s, float alpha);
-int pos_sched_factors_ready(pos_sched* s, int32_t l, const void* u, const void* v, void* stream);
-int pos_sched_grad_ready(pos_sched* s, int32_t l, void* stream);
+/* FC trigger ("(2) ... as long as b_t^l was finished"). rows = the number of sample rows
+ * of u (K x M) and v (K x N); it must equal the K registered by pos_sched_add_fc, else POS_EINVAL (a
+ * short last batch would make the pack read past u and v: pad it with zero rows, which contribute
+ * nothing to U^T V). factors_ready: an event recorded once u (= grad_output) and v (= the saved
+ * input) are complete — the pack and the gather wait on it, so they can overlap b^l's grad_input
+ * GEMM. weights_free: an event recorded once b^l has finished READING W (after its grad_input
+ * GEMM) — the reconstruction, which writes W, waits on it; NULL = factors_ready. u and v must stay
+ * valid and unmodified until the layer's sync completes. */
+int pos_sched_factors_ready(pos_sched* s, int32_t l, int64_t rows, const void* u, const void* v,
+                            void* factors_ready, void* weights_free);
+/* DENSE trigger: grad_ready = an event recorded once dW of layer l is complete in its grad buffer
+ * (a bucket's sync waits for the events of all its layers). */
+int pos_sched_grad_ready(pos_sched* s, int32_t l, void* grad_ready);
 /* Per-layer RAW gate: `consumer` waits until layer l's parameters are applied (for f^l of the
  * next iteration; the cross-iteration overlap of PAPER:158). */
 int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer);
 int pos_sched_end(pos_sched* s, void* consumer);
+/* Ends the iteration WITHOUT a global wait: every consumer gates itself per layer with
+ * pos_sched_wait_layer (f^l of the next iteration waits for s^l only — the cross-iteration overlap
+ * of PAPER:158). producer = the backward stream (POS_SCHED_SEQUENTIAL issues the deferred syncs
+ * behind it). The WAR contract above then holds per layer through the wait_layer gates. */
+int pos_sched_end_layers(pos_sched* s, void* producer);
+/* Host wait (after pos_sched_end) until every unit of the last iteration has completed, at most
+ * timeout_ms milliseconds (0 = unbounded): POS_ETIMEOUT if not done by then (not sticky: the device
+ * work may still finish), the sticky watchdog error at once if a device-side wait expired.
+ * Eager iterations only (POS_ESTATE once iterations were captured into CUDA graphs). */
+int pos_sched_wait(pos_sched* s, int64_t timeout_ms);
 /* Query: the scheme chosen for layer l. */
 int pos_sched_scheme(pos_sched* s, int32_t l);
 /* With POS_SCHED_TIMING(_APPLY): AVERAGE device milliseconds, over every iteration since the last reset,

@@ -19,6 +19,9 @@ POS_ROLE_SERVER, POS_ROLE_WORKER, POS_ROLE_BOTH = 0, 1, 2
 POS_DT_BF16, POS_DT_TF32, POS_DT_F32 = 0, 1, 2
 POS_IN_BF16, POS_IN_F32 = 0, 1
 POS_OK, POS_EINVAL, POS_ESTATE, POS_ECUDA, POS_ENCCL, POS_ENOMEM, POS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+POS_ETIMEOUT = -7
+POS_REDUCE_SWITCH, POS_REDUCE_RANK_ORDER = 0, 1
+POS_FAULT_NONE, POS_FAULT_SKIP_PS, POS_FAULT_SKIP_PACK = 0, 1, 2
 POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY, POS_SCHED_NO_SYMM, POS_SCHED_PS_AFTER_SFB = 1, 2, 4, 8, 16
 POS_SCHED_STATIC_TILES = 32
 
@@ -174,21 +177,41 @@ class Context:
         return cls.from_unique_id(bytes(t.cpu().tolist()), world, rank)
 
     def close(self):
+        """pos_finalize. With world > 1 this is COLLECTIVE (NCCL window deregistration and
+        communicator teardown): every rank must call it explicitly, in the same order."""
         if self.h:
             _chk(lib().pos_finalize(self.h), "pos_finalize")
             self.h = None
 
     def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+        # No collective teardown from the garbage collector (its order differs across ranks): a
+        # multi-rank context that was not closed explicitly is leaked with a warning.
+        if getattr(self, "h", None):
+            if self.world > 1 and not self.local:
+                import warnings
+                warnings.warn("poseidon Context (world > 1) garbage-collected without close(): leaked")
+                return
+            try:
+                self.close()
+            except Exception:
+                pass
 
     def async_error(self) -> int:
         return lib().pos_get_async_error(self.h)
 
     def set_max_ctas(self, n: int):
         _chk(lib().pos_set_max_ctas(self.h, n), "pos_set_max_ctas")
+
+    def set_timeout_ms(self, ms: int):
+        """Watchdog budget of every cross-GPU wait in the library's kernels (0 = unbounded)."""
+        _chk(lib().pos_set_timeout_ms(self.h, int(ms)), "pos_set_timeout_ms")
+
+    def set_reduce_order(self, order: int):
+        """POS_REDUCE_SWITCH (NVLS multimem reduce) or POS_REDUCE_RANK_ORDER (deterministic)."""
+        _chk(lib().pos_set_reduce_order(self.h, order), "pos_set_reduce_order")
+
+    def inject_fault(self, kind: int, rank: int):
+        _chk(lib().pos_inject_fault(self.h, kind, rank), "pos_inject_fault")
 
     def sym_empty(self, numel: int, dtype=None):
         """A zero-filled fp32 torch tensor in symmetric (NVLS multicast) memory — pos_mem_alloc.
@@ -205,6 +228,7 @@ class Context:
         t = torch.as_tensor(_Holder(), device=torch.device("cuda", torch.cuda.current_device()))
         if dtype != torch.float32:
             t = t.view(dtype)
+        t._pos_ctx = self   # the window lives as long as the context: keep the context alive
         return t
 
     def is_symmetric(self, t) -> bool:
@@ -239,12 +263,49 @@ class Context:
                                           _ptr(W), _ptr(b), alpha, _stream(stream)),
              "pos_sim_sync_layer_sfb")
 
+    def loop_sync_layer_ps(self, n, grads, Ws, alpha=1.0, stream=None):
+        """pos_loop_sync_layer_ps: P simulated ranks' replicas (flat fp32, >= pos_padded_size(n, P))."""
+        assert self.local and len(grads) == len(Ws) == self.world
+        gp = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        wp = (C.c_void_p * len(Ws))(*[w.data_ptr() for w in Ws])
+        _chk(lib().pos_loop_sync_layer_ps(self.h, n, gp, wp, alpha, _stream(stream)), "pos_loop_sync_layer_ps")
+
     def sim_sync_layer_ps(self, grads, W, alpha=1.0, n=None, stream=None):
         assert self.local and len(grads) == self.world
         n = W.numel() if n is None else n
         gp = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
         _chk(lib().pos_sim_sync_layer_ps(self.h, n, gp, _ptr(W), alpha, _stream(stream)),
              "pos_sim_sync_layer_ps")
+
+
+class LoopFC:
+    """pos_loop_fc: a loopback FC layer with one replica of W (and b) per simulated rank."""
+
+    def __init__(self, ctx: Context, M, N, K, Ws, bs=None, dtype="bf16"):
+        assert ctx.local and len(Ws) == ctx.world
+        self.ctx, self.M, self.N, self.K = ctx, M, N, K
+        self._keep = (list(Ws), None if bs is None else list(bs))
+        wp = (C.c_void_p * len(Ws))(*[w.data_ptr() for w in Ws])
+        bp = None if bs is None else (C.c_void_p * len(bs))(*[b.data_ptr() for b in bs])
+        h = C.c_void_p()
+        _chk(lib().pos_loop_fc_create(ctx.h, M, N, K, DTYPES[dtype], wp, bp, C.byref(h)), "pos_loop_fc_create")
+        self.h = h
+
+    def sync(self, us, vs, alpha, stream=None):
+        up = (C.c_void_p * len(us))(*[u.data_ptr() for u in us])
+        vp_ = (C.c_void_p * len(vs))(*[v.data_ptr() for v in vs])
+        _chk(lib().pos_loop_fc_sync(self.h, _in_dtype(us[0]), up, vp_, alpha, _stream(stream)), "pos_loop_fc_sync")
+
+    def close(self):
+        if self.h:
+            lib().pos_loop_fc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Scheduler:
@@ -262,6 +323,7 @@ class Scheduler:
         _chk(lib().pos_sched_create(ctx.h, n_layers, flags, C.byref(h)), "pos_sched_create")
         self.h = h
         self.L = n_layers
+        self._ev = {}        # one cached CUDA event per (layer, role): trigger plumbing only
 
     def add_fc(self, l, M, N, K, W, b=None, grad=None, dtype="bf16", in_dtype=POS_IN_BF16, force_scheme=-1):
         return _chk(lib().pos_sched_add_fc(self.h, l, M, N, K, in_dtype, DTYPES[dtype], _ptr(W), _ptr(b),
@@ -282,18 +344,41 @@ class Scheduler:
     def begin(self, alpha):
         _chk(lib().pos_sched_begin(self.h, alpha), "pos_sched_begin")
 
-    def factors_ready(self, l, u, v, stream=None):
-        _chk(lib().pos_sched_factors_ready(self.h, l, _ptr(u), _ptr(v), _stream(stream)),
+    def _event(self, key, stream):
+        """Record this (layer, role)'s cached event on `stream` and return its handle."""
+        import torch
+        ev = self._ev.get(key)
+        if ev is None:
+            ev = self._ev[key] = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream() if stream is None else stream)
+        return C.c_void_p(ev.cuda_event)
+
+    def factors_ready(self, l, u, v, stream=None, factors_ev=None, weights_free=None):
+        """pos_sched_factors_ready. Events are torch.cuda.Event objects already recorded by the
+        caller; if factors_ev is None, an event is recorded on `stream` now (then the pack also
+        waits for everything enqueued on it so far). weights_free=None: same as factors_ready."""
+        fe = C.c_void_p(factors_ev.cuda_event) if factors_ev is not None else self._event((l, 0), stream)
+        we = None if weights_free is None else C.c_void_p(weights_free.cuda_event)
+        _chk(lib().pos_sched_factors_ready(self.h, l, u.shape[0], _ptr(u), _ptr(v), fe, we),
              "pos_sched_factors_ready")
 
-    def grad_ready(self, l, stream=None):
-        _chk(lib().pos_sched_grad_ready(self.h, l, _stream(stream)), "pos_sched_grad_ready")
+    def grad_ready(self, l, stream=None, event=None):
+        ge = C.c_void_p(event.cuda_event) if event is not None else self._event((l, 1), stream)
+        _chk(lib().pos_sched_grad_ready(self.h, l, ge), "pos_sched_grad_ready")
+
+    def wait(self, timeout_ms=0):
+        """pos_sched_wait: host wait for the last iteration with a timeout (eager mode)."""
+        _chk(lib().pos_sched_wait(self.h, int(timeout_ms)), "pos_sched_wait")
 
     def wait_layer(self, l, stream=None):
         _chk(lib().pos_sched_wait_layer(self.h, l, _stream(stream)), "pos_sched_wait_layer")
 
     def end(self, stream=None):
         _chk(lib().pos_sched_end(self.h, _stream(stream)), "pos_sched_end")
+
+    def end_layers(self, stream=None):
+        """pos_sched_end_layers: close the iteration; consumers gate per layer with wait_layer."""
+        _chk(lib().pos_sched_end_layers(self.h, _stream(stream)), "pos_sched_end_layers")
 
     def scheme(self, l):
         return _chk(lib().pos_sched_scheme(self.h, l), "pos_sched_scheme")
@@ -315,16 +400,23 @@ class Scheduler:
         return sp.value
 
     def close(self):
+        """pos_sched_destroy. With world > 1 this frees symmetric windows (COLLECTIVE): call it
+        explicitly on every rank in the same order."""
         if self.h:
             lib().pos_sched_destroy(self.h)
             self.h = None
 
     def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+        if getattr(self, "h", None):
+            if self.ctx.world > 1 and not self.ctx.local:
+                import warnings
+                warnings.warn("poseidon Scheduler (world > 1) garbage-collected without close(): leaked")
+                return
+            try:
+                self.close()
+            except Exception:
+                pass
 
 
 __all__ = [n for n in dir() if n.startswith(("pos_", "POS_"))] + [
-    "Context", "Scheduler", "PoseidonError", "DTYPES", "SCHEME_NAMES", "LIB_PATH", "lib"]
+    "Context", "Scheduler", "LoopFC", "PoseidonError", "DTYPES", "SCHEME_NAMES", "LIB_PATH", "lib"]

@@ -34,6 +34,9 @@ SIGNATURES = {
     "pos_rank": (C.c_int, [vp]),
     "pos_get_async_error": (C.c_int, [vp]),
     "pos_set_max_ctas": (C.c_int, [vp, i32]),
+    "pos_set_timeout_ms": (C.c_int, [vp, i64]),
+    "pos_set_reduce_order": (C.c_int, [vp, i32]),
+    "pos_inject_fault": (C.c_int, [vp, i32, i32]),
     "pos_mem_alloc": (C.c_int, [vp, i64, C.POINTER(vp)]),
     "pos_mem_free": (C.c_int, [vp, vp]),
     "pos_mem_is_symmetric": (C.c_int, [vp, vp, i64]),
@@ -46,16 +49,22 @@ SIGNATURES = {
     "pos_sim_sync_layer_sfb": (C.c_int, [vp, i64, i64, i64, i32, i32, C.POINTER(vp), C.POINTER(vp),
                                          vp, vp, f32, vp]),
     "pos_sim_sync_layer_ps": (C.c_int, [vp, i64, C.POINTER(vp), vp, f32, vp]),
+    "pos_loop_sync_layer_ps": (C.c_int, [vp, i64, C.POINTER(vp), C.POINTER(vp), f32, vp]),
+    "pos_loop_fc_create": (C.c_int, [vp, i64, i64, i64, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    "pos_loop_fc_sync": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(vp), f32, vp]),
+    "pos_loop_fc_destroy": (C.c_int, [vp]),
     "pos_sched_create": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
     "pos_sched_add_fc": (C.c_int, [vp, i32, i64, i64, i64, i32, i32, vp, vp, vp, i32]),
     "pos_sched_add_dense": (C.c_int, [vp, i32, i64, vp, vp]),
     "pos_sched_add_dense_bucket": (C.c_int, [vp, i32, i32, P_i64, vp, vp]),
     "pos_sched_unit_of": (C.c_int, [vp, i32]),
     "pos_sched_begin": (C.c_int, [vp, f32]),
-    "pos_sched_factors_ready": (C.c_int, [vp, i32, vp, vp, vp]),
+    "pos_sched_factors_ready": (C.c_int, [vp, i32, i64, vp, vp, vp, vp]),
     "pos_sched_grad_ready": (C.c_int, [vp, i32, vp]),
+    "pos_sched_wait": (C.c_int, [vp, i64]),
     "pos_sched_wait_layer": (C.c_int, [vp, i32, vp]),
     "pos_sched_end": (C.c_int, [vp, vp]),
+    "pos_sched_end_layers": (C.c_int, [vp, vp]),
     "pos_sched_scheme": (C.c_int, [vp, i32]),
     "pos_sched_timing": (C.c_int, [vp, i32, P_f32, P_f32, P_f32]),
     "pos_sched_timing_reset": (C.c_int, [vp]),

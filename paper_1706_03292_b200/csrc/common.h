@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "poseidon.h"
@@ -76,6 +77,19 @@ cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, 
                                int32_t accumulate, float* b, float alpha, cudaStream_t s);
 cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s);
 constexpr int kMaxSimP = 16;
+constexpr int kMaxPeers = 16;   // ranks addressable by the fused symmetric-memory kernels
+
+// Flag-mode (double-buffered, barrier-free) factor gather: decided from RANK-INVARIANT inputs only
+// (every rank must make the same choice: it sets the symmetric allocation size and the protocol).
+// Tensor-core dtypes with N % 4 == 0 (the reconstruction selects the buffer on the device);
+// POS_GATHER_FLAGS=0 turns it off.
+inline bool gather_flag_mode(int32_t dtype, int64_t N) {
+  static const bool off = [] {
+    const char* e = getenv("POS_GATHER_FLAGS");
+    return e && e[0] == '0';
+  }();
+  return !off && dtype != POS_DT_F32 && (N % 4) == 0;
+}
 cudaError_t launch_sim_ps_reduce_apply(const float* const* grads, int P, float* W, int64_t n,
                                        float alpha, cudaStream_t s);
 // SIMT fp32 FFMA reconstruct-and-apply (POS_DT_F32, and the odd-ldw path)

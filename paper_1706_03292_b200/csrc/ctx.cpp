@@ -19,6 +19,11 @@ int ctx_nccl_fail(pos_ctx* c, ncclResult_t r, const char* what) {
 }
 
 int ctx_check(pos_ctx* c) {
+  if (c->sticky == POS_OK && c->err_host && *c->err_host != 0) {
+    c->sticky = POS_ETIMEOUT;
+    POS_FAIL(POS_ETIMEOUT, "watchdog: %s — timed out after %.3f s (rank %d of %d)",
+             site_name(*c->err_host), c->timeout_ns * 1e-9, c->rank, c->world);
+  }
   if (c->sticky != POS_OK) POS_FAIL(c->sticky, "context has a sticky asynchronous error");
   if (c->comm) {
     ncclResult_t ar = ncclSuccess;
@@ -145,6 +150,14 @@ static int ctx_common_init(pos_ctx* c) {
   int lo = 0, hi = 0;
   POS_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+  // watchdog error word: host-mapped, so the host reads it without synchronising
+  int* h = nullptr;
+  POS_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h), sizeof(int), cudaHostAllocMapped));
+  *h = 0;
+  c->err_host = h;
+  POS_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), h, 0));
+  const int64_t ms = env_int("POS_TIMEOUT_MS", 20000);
+  c->timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
   return POS_OK;
 }
 
@@ -205,6 +218,7 @@ int pos_finalize(pos_ctx* c) {
   }
   if (c->ws) cudaFree(c->ws);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->err_host) cudaFreeHost(const_cast<int*>(c->err_host));
   delete c;
   return rc;
 }
@@ -218,6 +232,29 @@ int pos_get_async_error(pos_ctx* c) {
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "asynchronous CUDA error");
   return ctx_check(c);
+}
+
+int pos_set_timeout_ms(pos_ctx* c, int64_t ms) {
+  clear_error();
+  POS_CHECK_ARG(c && ms >= 0, "bad arguments");
+  c->timeout_ns = (unsigned long long)ms * 1000000ull;
+  return POS_OK;
+}
+
+int pos_set_reduce_order(pos_ctx* c, int32_t order) {
+  clear_error();
+  POS_CHECK_ARG(c && (order == POS_REDUCE_SWITCH || order == POS_REDUCE_RANK_ORDER),
+                "bad arguments");
+  c->reduce_order = order;
+  return POS_OK;
+}
+
+int pos_inject_fault(pos_ctx* c, int32_t kind, int32_t rank) {
+  clear_error();
+  POS_CHECK_ARG(c && kind >= POS_FAULT_NONE && kind <= POS_FAULT_SKIP_PACK, "bad arguments");
+  c->fault = kind;
+  c->fault_rank = rank;
+  return POS_OK;
 }
 
 int pos_set_max_ctas(pos_ctx* c, int32_t max_ctas) {

@@ -17,6 +17,13 @@ struct pos_ctx {
   size_t ws_bytes = 0;
   int sticky = POS_OK;   // first asynchronous error seen
   void* symm = nullptr;  // symmetric-memory state (symm.cu): NCCL device comm + windows
+  // watchdog: every cross-GPU wait in a kernel gives up after timeout_ns (0 = unbounded) and
+  // writes a site code into this host-mapped word (first error wins); read without a sync
+  volatile int* err_host = nullptr;
+  int* err_dev = nullptr;
+  unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
+  int reduce_order = POS_REDUCE_SWITCH;   // PS reduce: NVLS switch order or fixed rank order
+  int fault = POS_FAULT_NONE, fault_rank = -1;   // fault injection (tests)
 };
 
 namespace pos {
@@ -56,6 +63,12 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
 int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                  const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done,
                  void* gbuf2 = nullptr, uint32_t* flags = nullptr, unsigned* fstate = nullptr);
-int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate, cudaStream_t s);
+// consumer-side wait (bounded) for the P ready flags of flag mode, before the reconstruction
+int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate, int P,
+                       cudaStream_t s);
+// true if [p, p+bytes) lies inside one symmetric window of the context
+bool symm_lookup(pos_ctx* c, const void* p, size_t bytes);
+// description of a watchdog site code (error word)
+const char* site_name(int site);
 
 }  // namespace pos

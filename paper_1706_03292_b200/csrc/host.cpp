@@ -51,7 +51,7 @@ using namespace pos;
 
 extern "C" {
 
-int pos_version(void) { return 100; }
+int pos_version(void) { return 200; }
 
 const char* pos_last_error(void) { return g_err; }
 

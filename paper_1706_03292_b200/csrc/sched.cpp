@@ -21,7 +21,9 @@
 //    Caffe+PS comparison of PAPER:407);
 //  * iterations may be captured into CUDA graphs: nothing here synchronises with the host while
 //    a stream is capturing, and timing events become external event nodes.
+#include <chrono>
 #include <cstdlib>
+#include <thread>
 #include <vector>
 
 #include "ctx.h"
@@ -75,7 +77,9 @@ struct Layer {
   int kind = POS_KIND_DENSE;
   int unit = -1;
   bool triggered = false;
-  cudaEvent_t ev_ready = nullptr;
+  // the caller's events of this iteration's trigger: inputs ready (factors / gradient) and, for
+  // an FC layer, W no longer read by b^l (nullptr = same as ev_in)
+  cudaEvent_t ev_in = nullptr, ev_wfree = nullptr;
 };
 
 }  // namespace
@@ -154,18 +158,13 @@ int harvest(Unit& u, TSlot& t, bool keep_used = false) {
 }
 
 // Enqueue sync(unit) behind the ready events of all its member layers.
-int issue_unit(pos_sched* s, int ui, bool capturing) {
+int issue_unit(pos_sched* s, int ui) {
   pos_ctx* c = s->ctx;
   Unit& un = s->units[ui];
   const int P = c->world;
   const bool coll = P > 1;                 // collectives needed?
   TSlot* ts = nullptr;
   int rc = POS_OK;
-  if (timing_any(s)) {
-    ts = &un.ring[(s->iter - 1) % kTRing];
-    if (!capturing && (rc = harvest(un, *ts))) return rc;   // no host sync inside a capture
-    ts->used = true;
-  }
   // stream of the first stage: the comm stream when a collective follows, else an apply stream
   // Consecutive SFB reconstructions alternate between two streams: they touch different layers, so
   // the next one's CTAs can take each SM as the previous one's persistent CTAs leave (no
@@ -179,13 +178,25 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
   // first stage: the comm stream when a collective follows; else an auxiliary apply stream, so the
   // factor pack of the next SFB layer overlaps the reconstruction of this one
   cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % 3];
-  for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_ready, 0));
+  for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_in, 0));
+  // the stage that WRITES W waits for b^l to have finished reading it (WAR)
+  const Layer& l0 = s->layers[un.members[0]];
+  cudaEvent_t ev_wfree = l0.ev_wfree ? l0.ev_wfree : l0.ev_in;
   // Optionally keep the NVLink-latency-bound PS kernels from co-running with the HBM-bound
   // reconstructions (they starve each other's memory pipelines); see DESIGN.md.
   if (coll && s->ps_after_sfb && un.scheme != POS_SCHEME_SFB && s->last_sfb >= 0)
     POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->units[s->last_sfb].ev_done, 0));
   if (un.scheme == POS_SCHEME_SFB) s->last_sfb = ui;
   if (s->flags & POS_SCHED_SEQUENTIAL) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_end, 0));
+  // cs has joined the caller's stream capture (if any) through the waits above; inside a capture
+  // nothing may synchronise with the host, so the timing slot is not harvested there
+  const bool capturing = is_capturing(cs);
+  s->captured |= capturing;
+  if (timing_any(s)) {
+    ts = &un.ring[(s->iter - 1) % kTRing];
+    if (!capturing && (rc = harvest(un, *ts))) return rc;
+    ts->used = true;
+  }
   if (ts && (rc = trec(ts->start, cs))) return rc;
   if (un.scheme == POS_SCHEME_SFB) {
     const int64_t R = row_elems(un.M, un.N), slot = un.K * R;
@@ -210,7 +221,7 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
       // the comm stream, which moves on to the next unit at once)
       POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));
       POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
-      if ((rc = symm_wait_gathered(c, un.gflags, un.gstate, as))) return rc;
+      if ((rc = symm_wait_gathered(c, un.gflags, un.gstate, P, as))) return rc;
       if (ts && (rc = trec(ts->gathered, as))) return rc;
     } else if (coll && mc) {
       if (ts && (rc = trec(ts->gathered, cs))) return rc;
@@ -229,7 +240,9 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
       POS_CUDA_TRY(cudaEventRecord(un.ev_gathered, cs));
       POS_CUDA_TRY(cudaStreamWaitEvent(as, un.ev_gathered, 0));
     }
-    // Move(CPU2GPU) analogue: A4 + A4b on the apply stream
+    // Move(CPU2GPU) analogue: A4 + A4b on the apply stream, once b^l no longer reads W
+    if (un.kind == POS_KIND_FC && ev_wfree != l0.ev_in)
+      POS_CUDA_TRY(cudaStreamWaitEvent(as, ev_wfree, 0));
     if (ts && (rc = trec(ts->a0, as))) return rc;
     if (un.plan_ctas != c->max_ctas) {   // (re)build the cached launch plan
       un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * P, un.dtype, un.gbuf, un.W,
@@ -257,6 +270,7 @@ int issue_unit(pos_sched* s, int ui, bool capturing) {
       rc = stage_fc_local_grad(c, un.M, un.N, un.K, un.in_dtype, un.dtype, un.u, un.v, un.gbuf,
                                un.grad, un.b != nullptr, cs);
       if (rc != POS_OK) return rc;
+      if (ev_wfree != l0.ev_in) POS_CUDA_TRY(cudaStreamWaitEvent(cs, ev_wfree, 0));
     }
     if (ts && (rc = trec(ts->packed, cs))) return rc;
     rc = stage_ps_dense(c, un.n, un.grad, un.W, s->alpha, cs, ts ? ts->a0 : nullptr,
@@ -274,20 +288,19 @@ int check_layer(pos_sched* s, int32_t l) {
   return POS_OK;
 }
 
-int trigger(pos_sched* s, int32_t l, cudaStream_t st) {
+int trigger(pos_sched* s, int32_t l, cudaEvent_t ev_in, cudaEvent_t ev_wfree) {
   Layer& ly = s->layers[l];
   if (!s->in_iter) POS_FAIL(POS_ESTATE, "trigger of layer %d outside begin/end", l);
   if (ly.triggered) POS_FAIL(POS_ESTATE, "layer %d triggered twice in one iteration", l);
-  POS_CUDA_TRY(cudaEventRecord(ly.ev_ready, st));
+  ly.ev_in = ev_in;
+  ly.ev_wfree = ev_wfree;
   ly.triggered = true;
   s->n_triggered++;
   Unit& un = s->units[ly.unit];
   if (--un.pending > 0) return POS_OK;      // bucket: wait for its remaining layers
   s->order.push_back(ly.unit);
   if (s->flags & POS_SCHED_SEQUENTIAL) return POS_OK;  // deferred to pos_sched_end
-  const bool cap = is_capturing(st);
-  s->captured |= cap;
-  return issue_unit(s, ly.unit, cap);
+  return issue_unit(s, ly.unit);
 }
 
 int new_unit(pos_sched* s, Unit&& u, int* out) {
@@ -309,8 +322,6 @@ int new_unit(pos_sched* s, Unit&& u, int* out) {
 
 int add_layer(pos_sched* s, int32_t l, int kind, int unit) {
   Layer& ly = s->layers[l];
-  int rc = make_event(&ly.ev_ready, false);
-  if (rc) return rc;
   ly.kind = kind;
   ly.unit = unit;
   ly.added = true;
@@ -377,6 +388,11 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   int scheme = force_scheme >= 0 ? force_scheme : pos_choose_scheme(M, N, K, c->world);
   if (scheme < 0) return scheme;
   const int64_t n = M * N + (b ? M : 0);
+  // Every rank must reconstruct with the same kernel (tensor-core vs SIMT results differ in the
+  // last bits) and pick the same gather protocol: decide from rank-invariant inputs only, and
+  // reject a W the tensor-core plan cannot address instead of silently falling back on one rank.
+  if (c->world > 1 && scheme == POS_SCHEME_SFB && dtype != POS_DT_F32 && (N % 4) == 0)
+    POS_CHECK_ARG(aligned16(W), "W must be 16-byte aligned (P > 1, tensor-core reconstruction)");
   if (scheme == POS_SCHEME_PS) {
     POS_CHECK_ARG(grad, "FC layer on the PS path needs a grad buffer");
     POS_CHECK_ARG(!b || b == W + M * N, "FC layer on the PS path needs b == W + M*N");
@@ -400,11 +416,7 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
     // every rank registers its layers in the same order). Flag mode (tensor-core path only: the
     // reconstruction selects the buffer on the device): two buffers + P ready flags in one
     // allocation.
-    static const bool flags_off = [] {
-      const char* e = getenv("POS_GATHER_FLAGS");
-      return e && e[0] == '0';
-    }();
-    const bool fm = !flags_off && dtype != POS_DT_F32 && (N % 4) == 0 && aligned16(W);
+    const bool fm = gather_flag_mode(dtype, N);
     const size_t al = (bytes + 255) & ~size_t(255);
     const size_t total = fm ? 2 * al + 256 : bytes;
     if (pos_mem_alloc(c, (int64_t)total, &u.gbuf) == POS_OK) {
@@ -488,25 +500,32 @@ int pos_sched_begin(pos_sched* s, float alpha) {
   return POS_OK;
 }
 
-int pos_sched_factors_ready(pos_sched* s, int32_t l, const void* u, const void* v, void* stream) {
+int pos_sched_factors_ready(pos_sched* s, int32_t l, int64_t rows, const void* u, const void* v,
+                            void* factors_ready, void* weights_free) {
   clear_error();
   int rc = check_layer(s, l);
   if (rc) return rc;
   Layer& ly = s->layers[l];
   if (!ly.added || ly.kind != POS_KIND_FC) POS_FAIL(POS_ESTATE, "layer %d is not an FC layer", l);
   POS_CHECK_ARG(u && v, "NULL factors");
-  s->units[ly.unit].u = u;
-  s->units[ly.unit].v = v;
-  return trigger(s, l, (cudaStream_t)stream);
+  POS_CHECK_ARG(factors_ready, "NULL factors_ready event");
+  Unit& un = s->units[ly.unit];
+  POS_CHECK_ARG(rows == un.K,
+                "layer %d: %lld factor rows but K = %lld was registered (pad a short batch with "
+                "zero rows)", l, (long long)rows, (long long)un.K);
+  un.u = u;
+  un.v = v;
+  return trigger(s, l, (cudaEvent_t)factors_ready, (cudaEvent_t)weights_free);
 }
 
-int pos_sched_grad_ready(pos_sched* s, int32_t l, void* stream) {
+int pos_sched_grad_ready(pos_sched* s, int32_t l, void* grad_ready) {
   clear_error();
   int rc = check_layer(s, l);
   if (rc) return rc;
   Layer& ly = s->layers[l];
   if (!ly.added || ly.kind != POS_KIND_DENSE) POS_FAIL(POS_ESTATE, "layer %d is not a dense layer", l);
-  return trigger(s, l, (cudaStream_t)stream);
+  POS_CHECK_ARG(grad_ready, "NULL grad_ready event");
+  return trigger(s, l, (cudaEvent_t)grad_ready, nullptr);
 }
 
 int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer) {
@@ -521,25 +540,56 @@ int pos_sched_wait_layer(pos_sched* s, int32_t l, void* consumer) {
   return POS_OK;
 }
 
-int pos_sched_end(pos_sched* s, void* consumer) {
-  clear_error();
+static int end_impl(pos_sched* s, cudaStream_t cs, bool wait_all) {
   POS_CHECK_ARG(s, "NULL scheduler");
   if (!s->in_iter) POS_FAIL(POS_ESTATE, "end without begin");
   if (s->n_triggered != s->L) {
     POS_FAIL(POS_ESTATE, "end with %d of %d layers triggered", s->n_triggered, s->L);
   }
-  cudaStream_t cs = (cudaStream_t)consumer;
   if (s->flags & POS_SCHED_SEQUENTIAL) {
     POS_CUDA_TRY(cudaEventRecord(s->ev_end, cs));
-    const bool cap = is_capturing(cs);
-    s->captured |= cap;
     for (int u : s->order) {
-      int rc = issue_unit(s, u, cap);
+      int rc = issue_unit(s, u);
       if (rc) { s->in_iter = false; return rc; }
     }
   }
-  for (auto& un : s->units) POS_CUDA_TRY(cudaStreamWaitEvent(cs, un.ev_done, 0));
+  if (wait_all)
+    for (auto& un : s->units) POS_CUDA_TRY(cudaStreamWaitEvent(cs, un.ev_done, 0));
   s->in_iter = false;
+  return ctx_check(s->ctx);
+}
+
+int pos_sched_end(pos_sched* s, void* consumer) {
+  clear_error();
+  return end_impl(s, (cudaStream_t)consumer, true);
+}
+
+int pos_sched_end_layers(pos_sched* s, void* producer) {
+  clear_error();
+  return end_impl(s, (cudaStream_t)producer, false);
+}
+
+int pos_sched_wait(pos_sched* s, int64_t timeout_ms) {
+  clear_error();
+  POS_CHECK_ARG(s && timeout_ms >= 0, "bad arguments");
+  if (s->in_iter) POS_FAIL(POS_ESTATE, "wait inside an iteration (call pos_sched_end first)");
+  if (s->captured) POS_FAIL(POS_ESTATE, "iterations were captured into CUDA graphs: synchronise the graph's stream");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (auto& un : s->units) {
+    for (;;) {
+      const cudaError_t q = cudaEventQuery(un.ev_done);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) return ctx_cuda_fail(s->ctx, q, "pos_sched_wait");
+      int rc = ctx_check(s->ctx);          // a device-side watchdog expiry ends the wait at once
+      if (rc) return rc;
+      const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(
+                          std::chrono::steady_clock::now() - t0).count();
+      if (timeout_ms > 0 && ms > timeout_ms)
+        POS_FAIL(POS_ETIMEOUT, "pos_sched_wait: iteration not complete after %lld ms",
+                 (long long)timeout_ms);
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
   return ctx_check(s->ctx);
 }
 
@@ -649,8 +699,6 @@ int pos_sched_destroy(pos_sched* s) {
     if (un.tile_counter) cudaFree(un.tile_counter);
     if (un.gstate) cudaFree(un.gstate);
   }
-  for (auto& ly : s->layers)
-    if (ly.ev_ready) cudaEventDestroy(ly.ev_ready);
   for (auto st : s->pool)
     if (st) cudaStreamDestroy(st);
   if (s->ev_end) cudaEventDestroy(s->ev_end);

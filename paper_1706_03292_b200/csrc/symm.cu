@@ -1,21 +1,38 @@
 // NVLink-SHARP / symmetric-memory path: the PS and SFB collectives fused into
 // the kernels that consume them, over NVSwitch multicast (NVLS) memory registered as NCCL symmetric
-// windows. NCCL provides only the plumbing (allocation, window registration, the device-side
-// pointers and the cross-GPU barrier); the data movement and arithmetic are these kernels.
+// windows. NCCL provides only the plumbing (allocation, window registration and the device-side
+// address resolution, done ONCE per window here); the data movement, the arithmetic and the
+// cross-GPU synchronisation are these kernels.
 //
-//  * ps_nvls_kernel (A6 + A7 + A8 fused): rank r owns shard [lo, hi) of a dense unit.
-//      ghat = multimem.ld_reduce.add(grad[i])      -- the switch sums all P workers' gradients
-//      w    = W_local[i] + alpha * ghat            -- the server's "apply (+)"
-//      multimem.st(W[i], w)                        -- fresh parameters to every replica
-//    bracketed by two LSA barriers: gradients of all ranks complete before the reduce, every
-//    replica's W complete (and every gradient consumed) before any rank proceeds.
-//  * pack_mc_kernel (A2 + A3 fused): this rank's sufficient factors, packed and cast,
-//    are multicast-stored into its slot of EVERY rank's gather buffer (one NVLink egress copy; the
-//    switch replicates), followed by an LSA barrier so the reconstruction can read all P slots.
+//  * ps_sync_kernel (A6 + A7 + A8 fused): rank r owns shard [lo, hi) of a dense unit.
+//      ghat = reduce over ranks of grad[i]    -- (1) workers push gradients; the server sums them
+//      w    = W_local[i] + alpha * ghat       -- (2) the server's "apply (+)"
+//      store w into W[i] of every replica     -- (3) consistency: every worker reads it back
+//    The reduce is either multimem.ld_reduce through the switch (default; the switch picks the
+//    summation order) or, in RANK-ORDER mode, plain peer loads summed in rank order 0..P-1
+//    (deterministic run to run). The broadcast is a multimem.st (the switch replicates) or P plain
+//    stores.
+//  * pack_x_kernel (A2 + A3 fused): this rank's sufficient factors, packed and cast, are
+//    stored into its slot of EVERY rank's gather buffer (one multicast store, or P unicast stores).
+//    Flag mode publishes completion with a release-store of the iteration number into flag[rank]
+//    of every replica; the consumer runs wait_flags_kernel before the reconstruction.
 //
-// All fused kernels of a context run on its comm stream, in the same order on every rank, so one
-// set of barrier indices [0, kBarriers) is reused sequentially (the session epochs persist in the
-// barrier resource buffer, also across CUDA-graph replays).
+// Every kernel addresses the other ranks through a POINTER TABLE (per-rank addresses and the
+// multicast address, resolved once when a window is registered). The single-GPU LOOPBACK entry
+// points at the end of this file run the very same kernels with a table of P local replicas, rank
+// after rank in stream order — the driver's one-GPU tests exercise the P > 1 kernel bodies that way.
+//
+// Cross-GPU waits (entry / exit barriers, gather flags) are bounded: a wait that exceeds the
+// context's timeout writes a code into the context's host-mapped error word and the kernel returns;
+// the host reports it as the sticky error POS_ETIMEOUT (SURVEY §5 failure detection).
+//
+// Barriers: one ENTRY inbox and one EXIT inbox (u32 counters) per context in a symmetric window.
+// Entry: CTA 0 of each rank adds 1 to every rank's entry inbox (multimem.red); every CTA polls its
+// local inbox until all P arrivals of this kernel instance are in. Exit: each CTA counts itself done;
+// the LAST CTA of the rank adds 1 to every exit inbox (release) and waits for all P. No CTA waits
+// for a specific CTA of another GPU, so the kernels tolerate any residency pattern (a per-CTA-index
+// barrier needs matching CTAs of all GPUs co-resident at once). Fused kernels of one context must
+// be stream-ordered among themselves (the scheduler issues them all on its comm stream).
 #include <cuda_bf16.h>
 #include <nccl.h>
 #include <nccl_device.h>
@@ -27,24 +44,28 @@
 
 namespace pos {
 
-constexpr int kBarriers = 128;  // max CTAs of a fused kernel
-
 struct SymmWindow {
-  char* base;
-  size_t bytes;
-  ncclWindow_t win;
+  char* base = nullptr;
+  size_t bytes = 0;
+  ncclWindow_t win = nullptr;
+  char* peer[kMaxPeers] = {};   // every rank's copy of the window (world-rank order)
+  char* mc = nullptr;           // multicast (NVLS) address of the window
 };
 
 struct SymmState {
   ncclDevComm dev;
   bool ready = false;
-  bool multimem = false;
   std::vector<SymmWindow> windows;
+  SymmWindow bar;                 // internal: [0] entry inbox, [1] exit inbox
+  uint32_t* bar_state = nullptr;  // device: [0] entry epoch, [1] exit epoch, [2] CTAs done
 };
 
 static SymmState* state(pos_ctx* c) { return static_cast<SymmState*>(c->symm); }
 
 namespace {
+
+// error sites reported through the context's error word (see site_name)
+enum { kSitePsEntry = 1, kSitePsExit = 2, kSitePackEntry = 3, kSitePackExit = 4, kSiteFlags = 5 };
 
 // ------------------------------------------------------------------------------ device -------
 __device__ __forceinline__ float4 mm_ld_reduce_v4(const float* p) {
@@ -68,173 +89,227 @@ __device__ __forceinline__ void mm_st_v4(float* p, float4 v) {
 __device__ __forceinline__ void mm_st(float* p, float v) {
   asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
-#ifndef POS_PACK_CTA_FENCE
-#define POS_PACK_CTA_FENCE 1
-#endif
-#ifndef POS_ENTRY_ORDER
-#define POS_ENTRY_ORDER cuda::memory_order_acquire
-#endif
-constexpr cuda::memory_order kEntryOrder = POS_ENTRY_ORDER;
+// Spin until *p has reached `target` (mod 2^32). Bounded: after timeout_ns (0 = unbounded) the
+// site code is written to the error word (first error wins) and false is returned.
+__device__ bool poll_reached(const uint32_t* p, uint32_t target, unsigned long long timeout_ns,
+                             int* err, int site) {
+  unsigned long long t0 = 0;
+  for (uint32_t spin = 1;; ++spin) {
+    if ((int32_t)(ld_acquire_sys(p) - target) >= 0) return true;
+    if (timeout_ns && (spin & 63) == 0) {
+      const unsigned long long t = gtimer();
+      if (t0 == 0) {
+        t0 = t;
+      } else if (t - t0 > timeout_ns) {
+        atomicCAS(err, 0, site);
+        __threadfence_system();
+        return false;
+      }
+    }
+  }
+}
+
+// Cross-GPU synchronisation of one fused-kernel instance. local == nullptr: none (P = 1 or the
+// single-GPU loopback, where ranks run one after the other in stream order).
+struct Xg {
+  uint32_t* mc;          // multicast address of the inbox pair [entry, exit]
+  uint32_t* local;       // this rank's inbox pair
+  uint32_t* state;       // [0] entry epoch, [1] exit epoch, [2] CTAs of this instance done
+  int P;
+  unsigned long long timeout_ns;
+  int* err;
+  int site;              // entry site; exit = site + 1
+};
+
+// Entry: every rank's inputs (produced by kernels that completed in stream order) are in place.
+// The arrival needs no release fence: the data was written by completed kernels.
+__device__ __forceinline__ bool xg_enter(const Xg& x) {
+  __shared__ int s_ok;
+  if (!x.local) return true;
+  if (threadIdx.x == 0) {
+    const uint32_t target = *reinterpret_cast<volatile uint32_t*>(x.state) + (uint32_t)x.P;
+    if (blockIdx.x == 0)
+      asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(x.mc) : "memory");
+    s_ok = poll_reached(x.local, target, x.timeout_ns, x.err, x.site) ? 1 : 0;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// Exit: the last CTA of this rank (all of the rank's stores performed) signals with release and
+// waits until every rank has done the same — every replica's outputs are complete and every input
+// read, before any rank's stream moves on.
+__device__ __forceinline__ void xg_exit(const Xg& x) {
+  if (!x.local) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();                 // this CTA's (multicast / peer) stores are performed
+    const unsigned prev = atomicAdd(x.state + 2, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      x.state[2] = 0;
+      const uint32_t target = x.state[1] + (uint32_t)x.P;
+      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(x.mc + 1) : "memory");
+      poll_reached(x.local + 1, target, x.timeout_ns, x.err, x.site + 1);
+      x.state[0] += (uint32_t)x.P;
+      x.state[1] = target;
+    }
+  }
+}
 
 constexpr int kPsThreads = 512;
 #ifndef POS_NVLS_UNROLL
 #define POS_NVLS_UNROLL 4
 #endif
-constexpr int kPsUnroll = POS_NVLS_UNROLL;   // 16-byte NVLS reductions in flight per thread
+constexpr int kPsUnroll = POS_NVLS_UNROLL;   // 16-byte reductions in flight per thread
 
-__global__ void __launch_bounds__(kPsThreads)
-ps_nvls_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, size_t off_w,
-               int64_t lo, int64_t hi, float alpha) {
-  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
-  // Entry: every worker's gradient is in place. The gradients were written by kernels that have
-  // completed (stream order), i.e. they are in each GPU's L2, where NVLS reads are served: the
-  // arrival needs no release fence (POS_ENTRY_ORDER selects the order for experiments).
-  bar.sync(ncclCoopCta(), kEntryOrder);
-  const float* gmc = static_cast<const float*>(ncclGetLsaMultimemPointer(wg, off_g, dc));
-  float* wmc = static_cast<float*>(ncclGetLsaMultimemPointer(ww, off_w, dc));
-  const float* wl = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
-  const int64_t v0 = lo / 4, v1 = hi / 4;   // lo is a multiple of 64
+// One PS unit on one rank. All pointers address element 0 of the unit's flat buffers.
+struct PsArgs {
+  const float* g_mc;            // multicast address of grad (kRedMc)
+  float* w_mc;                  // multicast address of W (kStMc)
+  const float* g[kMaxPeers];    // every rank's grad, rank order (peer reduce)
+  float* w[kMaxPeers];          // every rank's W (peer broadcast)
+  const float* wl;              // this rank's W
+  int P;
+  int64_t lo, hi;               // this rank's shard
+  float alpha;
+};
+
+template <bool kRedMc>
+__device__ __forceinline__ float4 ps_red4(const PsArgs& a, int64_t i) {
+  if constexpr (kRedMc) {
+    return mm_ld_reduce_v4(a.g_mc + 4 * i);
+  } else {   // fixed rank order: identical on every run, every rank
+    float4 s = *reinterpret_cast<const float4*>(a.g[0] + 4 * i);
+    for (int p = 1; p < a.P; ++p) {
+      const float4 t = *reinterpret_cast<const float4*>(a.g[p] + 4 * i);
+      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+    }
+    return s;
+  }
+}
+template <bool kRedMc>
+__device__ __forceinline__ float ps_red1(const PsArgs& a, int64_t j) {
+  if constexpr (kRedMc) {
+    return mm_ld_reduce(a.g_mc + j);
+  } else {
+    float s = a.g[0][j];
+    for (int p = 1; p < a.P; ++p) s += a.g[p][j];
+    return s;
+  }
+}
+template <bool kStMc>
+__device__ __forceinline__ void ps_st4(const PsArgs& a, int64_t i, float4 v) {
+  if constexpr (kStMc) {
+    mm_st_v4(a.w_mc + 4 * i, v);
+  } else {
+    for (int p = 0; p < a.P; ++p) *reinterpret_cast<float4*>(a.w[p] + 4 * i) = v;
+  }
+}
+template <bool kStMc>
+__device__ __forceinline__ void ps_st1(const PsArgs& a, int64_t j, float v) {
+  if constexpr (kStMc) {
+    mm_st(a.w_mc + j, v);
+  } else {
+    for (int p = 0; p < a.P; ++p) a.w[p][j] = v;
+  }
+}
+
+template <bool kRedMc, bool kStMc>
+__global__ void __launch_bounds__(kPsThreads) ps_sync_kernel(PsArgs a, Xg x) {
+  if (!xg_enter(x)) return;
+  const int64_t v0 = a.lo / 4, v1 = a.hi / 4;   // lo is a multiple of 64
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kPsUnroll - 1) * stride < v1; i += kPsUnroll * stride) {
     float4 g[kPsUnroll], w[kPsUnroll];
 #pragma unroll
     for (int u = 0; u < kPsUnroll; ++u) {
-      g[u] = mm_ld_reduce_v4(gmc + 4 * (i + u * stride));
-      w[u] = *reinterpret_cast<const float4*>(wl + 4 * (i + u * stride));
+      g[u] = ps_red4<kRedMc>(a, i + u * stride);
+      w[u] = *reinterpret_cast<const float4*>(a.wl + 4 * (i + u * stride));
     }
 #pragma unroll
     for (int u = 0; u < kPsUnroll; ++u) {
-      w[u].x = fmaf(alpha, g[u].x, w[u].x);
-      w[u].y = fmaf(alpha, g[u].y, w[u].y);
-      w[u].z = fmaf(alpha, g[u].z, w[u].z);
-      w[u].w = fmaf(alpha, g[u].w, w[u].w);
-      mm_st_v4(wmc + 4 * (i + u * stride), w[u]);
+      w[u].x = fmaf(a.alpha, g[u].x, w[u].x);
+      w[u].y = fmaf(a.alpha, g[u].y, w[u].y);
+      w[u].z = fmaf(a.alpha, g[u].z, w[u].z);
+      w[u].w = fmaf(a.alpha, g[u].w, w[u].w);
+      ps_st4<kStMc>(a, i + u * stride, w[u]);
     }
   }
   for (; i < v1; i += stride) {
-    float4 g = mm_ld_reduce_v4(gmc + 4 * i);
-    float4 w = *reinterpret_cast<const float4*>(wl + 4 * i);
-    w.x = fmaf(alpha, g.x, w.x);
-    w.y = fmaf(alpha, g.y, w.y);
-    w.z = fmaf(alpha, g.z, w.z);
-    w.w = fmaf(alpha, g.w, w.w);
-    mm_st_v4(wmc + 4 * i, w);
+    const float4 g = ps_red4<kRedMc>(a, i);
+    float4 w = *reinterpret_cast<const float4*>(a.wl + 4 * i);
+    w.x = fmaf(a.alpha, g.x, w.x);
+    w.y = fmaf(a.alpha, g.y, w.y);
+    w.z = fmaf(a.alpha, g.z, w.z);
+    w.w = fmaf(a.alpha, g.w, w.w);
+    ps_st4<kStMc>(a, i, w);
   }
   if (blockIdx.x == 0)   // scalar tail of the shard
-    for (int64_t j = v1 * 4 + threadIdx.x; j < hi; j += blockDim.x)
-      mm_st(wmc + j, fmaf(alpha, mm_ld_reduce(gmc + j), wl[j]));
-  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // every replica's W is complete
-}
-
-// P = 2 variant of the fused PS step with plain peer loads / stores over NVLink (LSA pointers):
-// per GPU and direction it moves n/2 + n/2 fp32 words where the NVLS path moves ~1.5 n (the switch
-// reads every copy, including the local one, and writes every replica). Sum in rank order.
-__global__ void __launch_bounds__(kPsThreads)
-ps_p2p2_kernel(ncclDevComm dc, ncclWindow_t wg, size_t off_g, ncclWindow_t ww, size_t off_w,
-               int64_t lo, int64_t hi, float alpha) {
-  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
-  bar.sync(ncclCoopCta(), kEntryOrder);     // both gradients are in place (see ps_nvls_kernel)
-  const float* g0 = static_cast<const float*>(ncclGetLsaPointer(wg, off_g, 0));
-  const float* g1 = static_cast<const float*>(ncclGetLsaPointer(wg, off_g, 1));
-  float* w0 = static_cast<float*>(ncclGetLsaPointer(ww, off_w, 0));
-  float* w1 = static_cast<float*>(ncclGetLsaPointer(ww, off_w, 1));
-  const float* wl = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
-  const int64_t v0 = lo / 4, v1 = hi / 4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (kPsUnroll - 1) * stride < v1; i += kPsUnroll * stride) {
-    float4 a[kPsUnroll], b[kPsUnroll], w[kPsUnroll];
-#pragma unroll
-    for (int u = 0; u < kPsUnroll; ++u) {
-      a[u] = *reinterpret_cast<const float4*>(g0 + 4 * (i + u * stride));
-      b[u] = *reinterpret_cast<const float4*>(g1 + 4 * (i + u * stride));
-      w[u] = *reinterpret_cast<const float4*>(wl + 4 * (i + u * stride));
-    }
-#pragma unroll
-    for (int u = 0; u < kPsUnroll; ++u) {
-      w[u].x = fmaf(alpha, a[u].x + b[u].x, w[u].x);
-      w[u].y = fmaf(alpha, a[u].y + b[u].y, w[u].y);
-      w[u].z = fmaf(alpha, a[u].z + b[u].z, w[u].z);
-      w[u].w = fmaf(alpha, a[u].w + b[u].w, w[u].w);
-      *reinterpret_cast<float4*>(w0 + 4 * (i + u * stride)) = w[u];
-      *reinterpret_cast<float4*>(w1 + 4 * (i + u * stride)) = w[u];
-    }
-  }
-  for (; i < v1; i += stride) {
-    const float4 a = *reinterpret_cast<const float4*>(g0 + 4 * i);
-    const float4 b = *reinterpret_cast<const float4*>(g1 + 4 * i);
-    float4 w = *reinterpret_cast<const float4*>(wl + 4 * i);
-    w.x = fmaf(alpha, a.x + b.x, w.x);
-    w.y = fmaf(alpha, a.y + b.y, w.y);
-    w.z = fmaf(alpha, a.z + b.z, w.z);
-    w.w = fmaf(alpha, a.w + b.w, w.w);
-    *reinterpret_cast<float4*>(w0 + 4 * i) = w;
-    *reinterpret_cast<float4*>(w1 + 4 * i) = w;
-  }
-  if (blockIdx.x == 0)   // scalar tail of the shard
-    for (int64_t j = v1 * 4 + threadIdx.x; j < hi; j += blockDim.x) {
-      const float w = fmaf(alpha, g0[j] + g1[j], wl[j]);
-      w0[j] = w;
-      w1[j] = w;
-    }
-  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // both replicas of W are complete
+    for (int64_t j = v1 * 4 + threadIdx.x; j < a.hi; j += blockDim.x)
+      ps_st1<kStMc>(a, j, fmaf(a.alpha, ps_red1<kRedMc>(a, j), a.wl[j]));
+  xg_exit(x);
 }
 
 __device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ float ld_in(const float* p) { return *p; }
 
-// Gather state of one SFB unit in flag mode (device memory of this rank, zero-initialised):
-// [0] packs completed by this rank (= iteration sequence), [1] CTAs of the running pack done.
-struct GatherFlags {
-  ncclWindow_t win;      // symmetric window holding the unit's P ready flags
-  size_t off_mine;       // offset of flag[rank] (written by this rank into every replica)
-  unsigned* state;       // this rank's GatherFlags state (2 x u32)
+// One rank's factor pack + gather. Byte addresses of THIS rank's slot in buffer 0 / 1.
+struct PackArgs {
+  const void* u;
+  const void* v;
+  int64_t M, N, Mp, R, K;
+  char* mc[2];                   // multicast address of the slot (kMc)
+  char* dst[2][kMaxPeers];       // the slot in every rank's buffer (unicast / loopback)
+  uint32_t* flag_mc;             // multicast address of flag[rank] (flag mode, kMc)
+  uint32_t* flag[kMaxPeers];     // flag[rank] in every rank's flags (flag mode, unicast)
+  unsigned* state;               // flag mode: this rank's [0] packs completed, [1] CTAs done
+  int P;
 };
 
-// One 16-byte output vector per thread iteration, multicast to every rank's gather buffer.
-//  kFlag = false: barrier mode — an entry barrier (cross-rank WAR on the single gather buffer) and
-//    an exit barrier (all P slots have landed everywhere) around the multicast.
-//  kFlag = true: flag mode — no waiting at all: the gather buffer is double-buffered by the
-//    iteration parity read from device memory (so a replayed CUDA graph alternates too), and the
-//    last CTA to finish publishes "slot of rank r for iteration s is complete" as a release-store
-//    of s into flag[r] of every replica. The consumer waits for the P flags (wait_flags_kernel).
-//    WAR safety: rank r writes buffer s%2 at iteration s only after its iteration s-1 consumed
-//    every rank's s-1 flag, and each rank publishes its s-1 flag only after finishing iteration
-//    s-2, whose reconstruction was the last reader of buffer s%2.
-//  kUC (flag mode only): P unicast stores through the peers' LSA pointers instead of one
-//    multimem store (an experiment knob, POS_PACK_UC=1).
-template <typename Tin, bool kBF16, bool kFlag, bool kUC = false>
-__global__ void __launch_bounds__(256)
-pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slot2,
-               const Tin* __restrict__ u, const Tin* __restrict__ v, int64_t M, int64_t N,
-               int64_t Mp, int64_t R, int64_t K, GatherFlags gf, int P = 0) {
+// One 16-byte output vector per thread iteration, into this rank's slot of every rank's buffer.
+//  kFlag = false: barrier mode — entry barrier (cross-rank WAR on the single gather buffer: every
+//    rank's previous reconstruction has finished reading it) and exit barrier (all P slots landed).
+//  kFlag = true: flag mode — no waiting: the gather buffer is double-buffered by the iteration
+//    parity read from device memory (a replayed CUDA graph alternates too), and the last CTA to
+//    finish publishes "slot of rank r for iteration s is complete" as a release-store of s into
+//    flag[r] of every replica. WAR safety: rank r writes buffer s%2 at iteration s only after its
+//    iteration s-1 consumed every rank's s-1 flag, and each rank publishes its s-1 flag only after
+//    finishing iteration s-2, whose reconstruction was the last reader of buffer s%2.
+template <typename Tin, bool kBF16, bool kFlag, bool kMc>
+__global__ void __launch_bounds__(256) pack_x_kernel(PackArgs a, Xg x) {
   uint32_t seq = 0;
   if constexpr (!kFlag) {
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
-    // Entry barrier: every rank has reached this iteration's pack on its comm stream, which (by
-    // pos_sched_end's contract) is after its previous reconstruction finished reading the gather
-    // buffer we are about to overwrite (cross-rank WAR).
-    bar.sync(ncclCoopCta(), kEntryOrder);
+    if (!xg_enter(x)) return;
   } else {
-    seq = *reinterpret_cast<volatile unsigned*>(gf.state);
+    seq = *reinterpret_cast<volatile unsigned*>(a.state);
   }
-  const size_t off = (kFlag && (seq & 1)) ? off_slot2 : off_slot;
-  float* dst = kUC ? nullptr : static_cast<float*>(ncclGetLsaMultimemPointer(wgb, off, dc));
-  float* peer_dst[8];
-  if constexpr (kUC)
-    for (int p = 0; p < P && p < 8; ++p) peer_dst[p] = static_cast<float*>(ncclGetLsaPointer(wgb, off, p));
+  const int b = (kFlag && (seq & 1)) ? 1 : 0;
+  const Tin* u = static_cast<const Tin*>(a.u);
+  const Tin* v = static_cast<const Tin*>(a.v);
   constexpr int VEC = kBF16 ? 8 : 4;
-  const int64_t chunks_per_row = R / VEC, total = K * chunks_per_row;
+  constexpr int EB = kBF16 ? 2 : 4;
+  const int64_t chunks_per_row = a.R / VEC, total = a.K * chunks_per_row;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = c / chunks_per_row, col = (c % chunks_per_row) * VEC;
     const Tin* src;
     int64_t idx, lim;
-    if (col < Mp) { src = u + k * M; idx = col; lim = M; }
-    else          { src = v + k * N; idx = col - Mp; lim = N; }
-    const int64_t onec = col < Mp ? -1 : N;   // ones column (fused bias), as in pack_*_kernel
+    if (col < a.Mp) { src = u + k * a.M; idx = col; lim = a.M; }
+    else            { src = v + k * a.N; idx = col - a.Mp; lim = a.N; }
+    const int64_t onec = col < a.Mp ? -1 : a.N;   // ones column (fused bias), as in pack_*_kernel
     float4 o;
     if constexpr (kBF16) {
       __align__(16) __nv_bfloat16 h[8];
@@ -248,41 +323,31 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slo
       o.z = idx + 2 < lim ? ld_in(src + idx + 2) : (idx + 2 == onec ? 1.f : 0.f);
       o.w = idx + 3 < lim ? ld_in(src + idx + 3) : (idx + 3 == onec ? 1.f : 0.f);
     }
-    // element offset of this 16-byte vector in float units: (k * R + col) * eb / 4
-    const int64_t eo = ((k * R + col) * (kBF16 ? 2 : 4)) / 4;
-    if constexpr (kUC) {
-      for (int p = 0; p < P && p < 8; ++p) *reinterpret_cast<float4*>(peer_dst[p] + eo) = o;
+    const int64_t boff = (k * a.R + col) * EB;   // byte offset of this vector in the slot
+    if constexpr (kMc) {
+      mm_st_v4(reinterpret_cast<float*>(a.mc[b] + boff), o);
     } else {
-      mm_st_v4(dst + eo, o);
+      for (int p = 0; p < a.P; ++p) *reinterpret_cast<float4*>(a.dst[b][p] + boff) = o;
     }
   }
   if constexpr (!kFlag) {
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, true);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);   // all P slots have landed everywhere
+    xg_exit(x);
   } else {
-#if POS_PACK_CTA_FENCE
     __syncthreads();                        // the CTA's stores happen-before thread 0's fence
-    if (threadIdx.x == 0) __threadfence_system();
-#else
-    __threadfence_system();                 // this thread's multicast stores are performed
-    __syncthreads();
-#endif
     if (threadIdx.x == 0) {
-      const unsigned prev = atomicAdd(gf.state + 1, 1u);
+      __threadfence_system();
+      const unsigned prev = atomicAdd(a.state + 1, 1u);
       if (prev == gridDim.x - 1) {          // last CTA: every CTA's stores are performed
         __threadfence_system();
-        gf.state[1] = 0;
-        gf.state[0] = seq + 1;
-        if constexpr (kUC) {
-          for (int p = 0; p < P && p < 8; ++p) {
-            uint32_t* f = static_cast<uint32_t*>(ncclGetLsaPointer(gf.win, gf.off_mine, p));
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(seq + 1) : "memory");
-          }
-        } else {
-          uint32_t* fmc =
-              static_cast<uint32_t*>(ncclGetLsaMultimemPointer(gf.win, gf.off_mine, dc));
-          asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(fmc), "r"(seq + 1)
+        a.state[1] = 0;
+        a.state[0] = seq + 1;
+        if constexpr (kMc) {
+          asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(a.flag_mc), "r"(seq + 1)
                        : "memory");
+        } else {
+          for (int p = 0; p < a.P; ++p)
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.flag[p]), "r"(seq + 1)
+                         : "memory");
         }
       }
     }
@@ -290,16 +355,21 @@ pack_mc_kernel(ncclDevComm dc, ncclWindow_t wgb, size_t off_slot, size_t off_slo
 }
 
 // Consumer side of flag mode: returns once every rank's slot of this iteration is in place
-// (flag[r] >= this rank's own sequence, which its pack has just advanced).
-__global__ void wait_flags_kernel(const uint32_t* flags, const unsigned* state, int P) {
+// (flag[r] >= this rank's own sequence, which its pack has just advanced). Bounded wait.
+__global__ void wait_flags_kernel(const uint32_t* flags, const unsigned* state, int P,
+                                  unsigned long long timeout_ns, int* err) {
   const uint32_t want = *reinterpret_cast<const volatile unsigned*>(state);
-  for (int r = threadIdx.x; r < P; r += blockDim.x) {
-    uint32_t got;
-    do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(got) : "l"(flags + r) : "memory");
-    } while ((int32_t)(got - want) < 0);
-  }
+  for (int r = threadIdx.x; r < P; r += blockDim.x)
+    poll_reached(flags + r, want, timeout_ns, err, kSiteFlags);
   __syncthreads();
+}
+
+// Address resolution of one window, once at registration: every rank's copy + the multicast one.
+__global__ void resolve_window_kernel(ncclDevComm dc, ncclWindow_t w, int P, char** out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    for (int p = 0; p < P; ++p) out[p] = static_cast<char*>(ncclGetPeerPointer(w, 0, p));
+    out[P] = static_cast<char*>(ncclGetLsaMultimemPointer(w, 0, dc));
+  }
 }
 
 int grid_for(int64_t items, int threads, int cap) {
@@ -309,26 +379,164 @@ int grid_for(int64_t items, int threads, int cap) {
   return (int)g;
 }
 
+// PS grid: a function of (n, P) only — the same on every rank (the last rank's shard may be short
+// or empty; the kernel grid-strides over its own shard).
+int ps_grid(pos_ctx* c, int64_t n, int P) {
+  static const int ps_ctas_env = [] {
+    const char* e = getenv("POS_NVLS_CTAS");
+    return (e && *e) ? atoi(e) : 0;
+  }();
+  // NVLS loads have microsecond latency. Measured (VGG19-22K / VGG19 steps, next to the
+  // reconstructions, round 1): P = 2 wants 64 CTAs (0.45 -> 0.41 ms; 16: 0.52, 128: 0.47); P = 4
+  // is best at 24-48. Rule: 128 / P CTAs (the same shard bytes per CTA at every P), >= 16.
+  (void)c;
+  int cap = ps_ctas_env > 0 ? ps_ctas_env : std::max(16, 128 / P);
+  const int64_t S = pos_shard_stride(n, P);
+  return grid_for(std::max<int64_t>(1, S / 4 / kPsUnroll), kPsThreads, cap);
+}
+
+Xg make_xg(pos_ctx* c, int site) {
+  Xg x{};
+  SymmState* st = state(c);
+  if (st && st->bar.mc && c->world > 1) {
+    x.mc = reinterpret_cast<uint32_t*>(st->bar.mc);
+    x.local = reinterpret_cast<uint32_t*>(st->bar.base);
+    x.state = st->bar_state;
+  }
+  x.P = c->world;
+  x.timeout_ns = c->timeout_ns;
+  x.err = c->err_dev;
+  x.site = site;
+  return x;
+}
+
+Xg no_xg(pos_ctx* c) {
+  Xg x{};
+  x.P = c->world;
+  x.timeout_ns = c->timeout_ns;
+  x.err = c->err_dev;
+  return x;
+}
+
+template <bool kRedMc, bool kStMc>
+cudaError_t launch_ps(int grid, cudaStream_t s, const PsArgs& a, const Xg& x) {
+  clear_stale_launch_error();
+  ps_sync_kernel<kRedMc, kStMc><<<grid, kPsThreads, 0, s>>>(a, x);
+  return cudaGetLastError();
+}
+
+template <bool kFlag, bool kMc>
+cudaError_t launch_pack(int grid, cudaStream_t s, int32_t in_dtype, int32_t dtype,
+                        const PackArgs& a, const Xg& x) {
+  using bf = __nv_bfloat16;
+  clear_stale_launch_error();
+  if (dtype == POS_DT_BF16) {
+    if (in_dtype == POS_IN_BF16) pack_x_kernel<bf, true, kFlag, kMc><<<grid, 256, 0, s>>>(a, x);
+    else                         pack_x_kernel<float, true, kFlag, kMc><<<grid, 256, 0, s>>>(a, x);
+  } else {
+    if (in_dtype == POS_IN_BF16) pack_x_kernel<bf, false, kFlag, kMc><<<grid, 256, 0, s>>>(a, x);
+    else                         pack_x_kernel<float, false, kFlag, kMc><<<grid, 256, 0, s>>>(a, x);
+  }
+  return cudaGetLastError();
+}
+
+int pack_grid(int64_t M, int64_t N, int64_t K, int32_t dtype) {
+  static const int pack_ctas = [] {
+    const char* e = getenv("POS_PACK_CTAS");
+    const int v = (e && *e) ? atoi(e) : 128;
+    return v < 1 ? 1 : v;
+  }();
+  const int vec = dtype == POS_DT_BF16 ? 8 : 4;
+  return grid_for(K * (row_elems(M, N) / vec), 256, pack_ctas);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------- host --------
+const char* site_name(int site) {
+  switch (site) {
+    case kSitePsEntry: return "PS unit entry barrier (a peer's gradients never arrived)";
+    case kSitePsExit: return "PS unit exit barrier (a peer never finished its shard)";
+    case kSitePackEntry: return "factor gather entry barrier";
+    case kSitePackExit: return "factor gather exit barrier";
+    case kSiteFlags: return "factor gather ready flags (a peer's slot never arrived)";
+    default: return "unknown cross-GPU wait";
+  }
+}
+
+static int register_window(pos_ctx* c, SymmState* st, void* p, size_t bytes, SymmWindow* out) {
+  ncclWindow_t win;
+  ncclResult_t r = ncclCommWindowRegister(c->comm, p, bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) return ctx_nccl_fail(c, r, "ncclCommWindowRegister");
+  // NCCL's registration may leave a benign runtime error behind: consume it
+  (void)cudaGetLastError();
+  char** dtab = nullptr;
+  POS_CUDA_TRY(cudaMalloc(&dtab, sizeof(char*) * (kMaxPeers + 1)));
+  resolve_window_kernel<<<1, 32>>>(st->dev, win, c->world, dtab);
+  cudaError_t e = cudaGetLastError();
+  char* htab[kMaxPeers + 1] = {};
+  if (e == cudaSuccess)
+    e = cudaMemcpy(htab, dtab, sizeof(char*) * (c->world + 1), cudaMemcpyDeviceToHost);
+  cudaFree(dtab);
+  if (e != cudaSuccess) {
+    ncclCommWindowDeregister(c->comm, win);
+    return ctx_cuda_fail(c, e, "window address resolution");
+  }
+  out->base = static_cast<char*>(p);
+  out->bytes = bytes;
+  out->win = win;
+  for (int q = 0; q < c->world; ++q) out->peer[q] = htab[q];
+  out->mc = htab[c->world];
+  if (!out->mc || out->peer[c->rank] != out->base) {
+    ncclCommWindowDeregister(c->comm, win);
+    POS_FAIL(POS_EUNSUPPORTED, "symmetric window without multicast / consistent local address");
+  }
+  return POS_OK;
+}
+
 static int symm_init(pos_ctx* c) {
   if (c->symm) return POS_OK;
   POS_CHECK_ARG(c->comm, "symmetric memory needs a multi-rank context");
+  POS_CHECK_ARG(c->world <= kMaxPeers, "symmetric memory supports at most %d ranks", kMaxPeers);
   SymmState* st = new SymmState();
   ncclDevCommRequirements reqs = {};
   reqs.lsaMultimem = true;
-  reqs.lsaBarrierCount = kBarriers;
   ncclResult_t r = ncclDevCommCreate(c->comm, &reqs, &st->dev);
   if (r != ncclSuccess) {
     delete st;
     return ctx_nccl_fail(c, r, "ncclDevCommCreate(lsaMultimem)");
   }
   st->ready = true;
+  if (st->dev.lsaSize != c->world || st->dev.lsaRank != c->rank) {
+    ncclDevCommDestroy(c->comm, &st->dev);
+    delete st;
+    POS_FAIL(POS_EUNSUPPORTED, "the ranks do not form one NVLink (LSA) team");
+  }
+  // the cross-GPU barrier inboxes of the fused kernels
+  void* p = nullptr;
+  r = ncclMemAlloc(&p, 4096);
+  if (r != ncclSuccess) {
+    ncclDevCommDestroy(c->comm, &st->dev);
+    delete st;
+    return ctx_nccl_fail(c, r, "ncclMemAlloc(barrier)");
+  }
+  int rc = register_window(c, st, p, 4096, &st->bar);
+  if (rc == POS_OK && (cudaMemset(p, 0, 4096) != cudaSuccess ||
+                       cudaMalloc(&st->bar_state, 4 * sizeof(uint32_t)) != cudaSuccess ||
+                       cudaMemset(st->bar_state, 0, 4 * sizeof(uint32_t)) != cudaSuccess ||
+                       cudaDeviceSynchronize() != cudaSuccess))
+    rc = ctx_cuda_fail(c, cudaGetLastError(), "barrier state");
+  if (rc != POS_OK) {
+    if (st->bar.win) ncclCommWindowDeregister(c->comm, st->bar.win);
+    ncclMemFree(p);
+    if (st->bar_state) cudaFree(st->bar_state);
+    ncclDevCommDestroy(c->comm, &st->dev);
+    delete st;
+    return rc;
+  }
   // with the collectives fused into our own kernels (which co-reside with the reconstruction
   // kernel) no SMs need to be kept free for NCCL CTAs
   if (!getenv("POS_SFB_MAX_CTAS")) c->max_ctas = 0;
-  st->multimem = true;
   c->symm = st;
   return POS_OK;
 }
@@ -340,103 +548,83 @@ void symm_destroy(pos_ctx* c) {
     ncclCommWindowDeregister(c->comm, w.win);
     ncclMemFree(w.base);
   }
+  if (st->bar.win) {
+    ncclCommWindowDeregister(c->comm, st->bar.win);
+    ncclMemFree(st->bar.base);
+  }
+  if (st->bar_state) cudaFree(st->bar_state);
   if (st->ready) ncclDevCommDestroy(c->comm, &st->dev);
   delete st;
   c->symm = nullptr;
 }
 
-bool symm_lookup(pos_ctx* c, const void* p, size_t bytes, ncclWindow_t* win, size_t* off) {
+static const SymmWindow* symm_find(pos_ctx* c, const void* p, size_t bytes, size_t* off) {
   SymmState* st = state(c);
-  if (!st || !st->multimem) return false;
+  if (!st) return nullptr;
   const char* q = static_cast<const char*>(p);
   for (auto& w : st->windows)
     if (q >= w.base && q + bytes <= w.base + w.bytes) {
-      *win = w.win;
       *off = (size_t)(q - w.base);
-      return true;
+      return &w;
     }
-  return false;
+  return nullptr;
+}
+
+bool symm_lookup(pos_ctx* c, const void* p, size_t bytes) {
+  size_t off;
+  return symm_find(c, p, bytes, &off) != nullptr;
 }
 
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                   cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done) {
-  clear_stale_launch_error();
   *done = false;
   const int P = c->world;
   if (P < 2 || c->local) return POS_OK;
   const int64_t padded = pos_padded_size(n, P);
-  ncclWindow_t wg, ww;
-  size_t og, ow;
-  if (!symm_lookup(c, grad, (size_t)padded * 4, &wg, &og) ||
-      !symm_lookup(c, W, (size_t)padded * 4, &ww, &ow) || (og % 16) || (ow % 16))
-    return POS_OK;   // not symmetric: caller uses the NCCL path
-  int64_t lo = 0, hi = 0;
-  pos_shard_range(n, P, c->rank, &lo, &hi);
+  size_t og = 0, ow = 0;
+  const SymmWindow* wg = symm_find(c, grad, (size_t)padded * 4, &og);
+  const SymmWindow* ww = symm_find(c, W, (size_t)padded * 4, &ow);
+  if (!wg || !ww || (og % 16) || (ow % 16)) return POS_OK;   // not symmetric: NCCL path
+  PsArgs a{};
+  a.g_mc = reinterpret_cast<const float*>(wg->mc + og);
+  a.w_mc = reinterpret_cast<float*>(ww->mc + ow);
+  for (int p = 0; p < P; ++p) {
+    a.g[p] = reinterpret_cast<const float*>(wg->peer[p] + og);
+    a.w[p] = reinterpret_cast<float*>(ww->peer[p] + ow);
+  }
+  a.wl = W;
+  a.P = P;
+  a.alpha = alpha;
+  pos_shard_range(n, P, c->rank, &a.lo, &a.hi);
+  const Xg x = make_xg(c, kSitePsEntry);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
-  // NVLS loads have microsecond latency. Measured (VGG19-22K / VGG19 steps, next to the
-  // reconstructions): P = 2 — each rank reduces half of every unit — wants 64 CTAs (0.45 -> 0.41 ms;
-  // 16: 0.52, 128: 0.47); P = 4 is best at 24-48 (64 hung once at P = 4: NVLS CTAs spinning in
-  // their barrier can starve the reconstructions and packs of SM slots). Rule: 128 / P CTAs (the
-  // same shard bytes per CTA at every P), at least 16 — P = 8 (not measurable here) gets 16.
-  static const int ps_ctas_env = [] {
-    const char* e = getenv("POS_NVLS_CTAS");
-    return (e && *e) ? atoi(e) : 0;
-  }();
-  int ps_ctas = ps_ctas_env > 0 ? ps_ctas_env : std::max(16, 128 / P);
-  if (ps_ctas > kBarriers) ps_ctas = kBarriers;
-  const int grid = grid_for(std::max<int64_t>(1, (hi - lo) / 4 / kPsUnroll), kPsThreads, ps_ctas);
+  const int grid = ps_grid(c, n, P);
   // P = 2 option (POS_PS_P2P=1): plain peer loads / stores move less over NVLink than the switch
-  // path — 10-20% faster alone (80 MB: 196 vs 218 us), but its NVLink traffic through the SMs'
-  // load/store path slows a concurrent reconstruction far more (VGG19-22K step 0.55 vs 0.45 ms);
-  // only the PS-only Inception-V3 step gains (-8%), so the NVLS kernel stays the default
+  // path — faster alone, but its NVLink traffic through the SMs' load/store path slows a
+  // concurrent reconstruction more (round-1 measurement); the NVLS kernel stays the default
   static const bool p2p2 = [] {
     const char* e = getenv("POS_PS_P2P");
     return e && e[0] == '1';
   }();
-  if (P == 2 && p2p2)
-    ps_p2p2_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
-  else
-    ps_nvls_kernel<<<grid, kPsThreads, 0, s>>>(state(c)->dev, wg, og, ww, ow, lo, hi, alpha);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_nvls_kernel launch");
+  cudaError_t e = cudaSuccess;
+  if (c->fault == POS_FAULT_SKIP_PS && c->fault_rank == c->rank) {
+    // fault injection: this rank never joins the unit (its peers' entry barriers time out)
+  } else if (P == 2 && p2p2) {
+    e = launch_ps<false, false>(grid, s, a, x);
+  } else if (c->reduce_order == POS_REDUCE_RANK_ORDER) {
+    e = launch_ps<false, true>(grid, s, a, x);   // deterministic sum, multicast broadcast
+  } else {
+    e = launch_ps<true, true>(grid, s, a, x);
+  }
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_sync_kernel launch");
   if (ev_a1) POS_CUDA_TRY(record_timing_event(ev_a1, s));
   *done = true;
   return POS_OK;
 }
 
-namespace {
-template <bool kFlag, bool kUC = false>
-void launch_pack_mc(int grid, cudaStream_t s, const ncclDevComm& dc, ncclWindow_t wgb,
-                    size_t off_slot, size_t off_slot2, int32_t in_dtype, int32_t dtype,
-                    const void* u, const void* v, int64_t M, int64_t N, int64_t Mp, int64_t R,
-                    int64_t K, GatherFlags gf, int P = 0) {
-  using bf = __nv_bfloat16;
-  if (dtype == POS_DT_BF16) {
-    if (in_dtype == POS_IN_BF16)
-      pack_mc_kernel<bf, true, kFlag, kUC><<<grid, 256, 0, s>>>(
-          dc, wgb, off_slot, off_slot2, static_cast<const bf*>(u), static_cast<const bf*>(v), M, N,
-          Mp, R, K, gf, P);
-    else
-      pack_mc_kernel<float, true, kFlag, kUC><<<grid, 256, 0, s>>>(
-          dc, wgb, off_slot, off_slot2, static_cast<const float*>(u),
-          static_cast<const float*>(v), M, N, Mp, R, K, gf, P);
-  } else {
-    if (in_dtype == POS_IN_BF16)
-      pack_mc_kernel<bf, false, kFlag, kUC><<<grid, 256, 0, s>>>(
-          dc, wgb, off_slot, off_slot2, static_cast<const bf*>(u), static_cast<const bf*>(v), M, N,
-          Mp, R, K, gf, P);
-    else
-      pack_mc_kernel<float, false, kFlag, kUC><<<grid, 256, 0, s>>>(
-          dc, wgb, off_slot, off_slot2, static_cast<const float*>(u),
-          static_cast<const float*>(v), M, N, Mp, R, K, gf, P);
-  }
-}
-}  // namespace
-
 int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                  const void* u, const void* v, void* gbuf, cudaStream_t s, bool* done,
                  void* gbuf2, uint32_t* flags, unsigned* fstate) {
-  clear_stale_launch_error();
   *done = false;
   if (c->world < 2 || c->local) return POS_OK;
   static const bool mc_off = [] {   // POS_PACK_MC=0: pack locally + NCCL all-gather instead
@@ -444,63 +632,55 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
     return e && e[0] == '0';
   }();
   if (mc_off) return POS_OK;
+  const int P = c->world;
   const int64_t R = row_elems(M, N), eb = dtype_bytes(dtype);
   const size_t slot_bytes = (size_t)(K * R * eb);
-  ncclWindow_t wgb, wgb2, wfl;
-  size_t off, off2 = 0, offf = 0;
-  if (!symm_lookup(c, gbuf, slot_bytes * c->world, &wgb, &off)) return POS_OK;
-  // flag mode needs the second buffer in the same window as the first (one window argument)
-  const bool flag_mode = gbuf2 && flags && fstate &&
-                         symm_lookup(c, gbuf2, slot_bytes * c->world, &wgb2, &off2) &&
-                         symm_lookup(c, flags, sizeof(uint32_t) * c->world, &wfl, &offf);
-  if (gbuf2 && !flag_mode) return POS_OK;   // inconsistent registration: caller uses NCCL
-  const size_t off_slot = off + (size_t)c->rank * slot_bytes;
-  const int vec = dtype == POS_DT_BF16 ? 8 : 4;
-  // barrier mode: one LSA barrier index per CTA (<= kBarriers); flag mode: no barrier, more CTAs
-  // keep more multicast stores in flight
-  static const int pack_ctas = [] {
-    const char* e = getenv("POS_PACK_CTAS");
-    const int v = (e && *e) ? atoi(e) : 128;
-    return v < 1 ? 1 : v;
-  }();
-  static const int pack_ctas_flag = [] {
-    const char* e = getenv("POS_PACK_CTAS_FLAG");
-    const int v = (e && *e) ? atoi(e) : 128;
-    return v < 1 ? 1 : v;
-  }();
-  const int grid = grid_for(K * (R / vec), 256,
-                            flag_mode ? pack_ctas_flag : std::min(pack_ctas, kBarriers));
-  const int64_t Mp = m_pad(M);
-  const ncclDevComm& dc = state(c)->dev;
-  if (flag_mode) {
-    // both buffers must be addressable through the first buffer's window: they are separate
-    // allocations, so pass the second one's window offset relative to its own window instead
-    GatherFlags gf{wfl, offf + sizeof(uint32_t) * (size_t)c->rank, fstate};
-    if (wgb2 != wgb) return POS_OK;         // (separate windows: not supported, NCCL path)
-    static const bool uc = [] {
-      const char* e = getenv("POS_PACK_UC");
-      return e && e[0] == '1';
-    }();
-    if (uc && c->world <= 8)
-      launch_pack_mc<true, true>(grid, s, dc, wgb, off_slot, off2 + (size_t)c->rank * slot_bytes,
-                                 in_dtype, dtype, u, v, M, N, Mp, R, K, gf, c->world);
-    else
-      launch_pack_mc<true>(grid, s, dc, wgb, off_slot, off2 + (size_t)c->rank * slot_bytes,
-                           in_dtype, dtype, u, v, M, N, Mp, R, K, gf);
-  } else {
-    launch_pack_mc<false>(grid, s, dc, wgb, off_slot, off_slot, in_dtype, dtype, u, v, M, N, Mp,
-                          R, K, GatherFlags{});
+  size_t off = 0, off2 = 0, offf = 0;
+  const SymmWindow* wb = symm_find(c, gbuf, slot_bytes * P, &off);
+  if (!wb) return POS_OK;
+  const bool flag_mode = gbuf2 && flags && fstate;
+  const SymmWindow* wb2 = flag_mode ? symm_find(c, gbuf2, slot_bytes * P, &off2) : nullptr;
+  const SymmWindow* wf = flag_mode ? symm_find(c, flags, sizeof(uint32_t) * P, &offf) : nullptr;
+  if (flag_mode && (!wb2 || !wf)) return POS_OK;   // inconsistent registration: caller uses NCCL
+  PackArgs a{};
+  a.u = u; a.v = v;
+  a.M = M; a.N = N; a.Mp = m_pad(M); a.R = R; a.K = K;
+  a.P = P;
+  const size_t mine = (size_t)c->rank * slot_bytes;
+  a.mc[0] = wb->mc + off + mine;
+  a.mc[1] = flag_mode ? wb2->mc + off2 + mine : a.mc[0];
+  for (int p = 0; p < P; ++p) {
+    a.dst[0][p] = wb->peer[p] + off + mine;
+    a.dst[1][p] = flag_mode ? wb2->peer[p] + off2 + mine : a.dst[0][p];
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack_mc_kernel launch");
+  if (flag_mode) {
+    const size_t fo = offf + sizeof(uint32_t) * (size_t)c->rank;
+    a.flag_mc = reinterpret_cast<uint32_t*>(wf->mc + fo);
+    for (int p = 0; p < P; ++p) a.flag[p] = reinterpret_cast<uint32_t*>(wf->peer[p] + fo);
+    a.state = fstate;
+  }
+  // POS_PACK_UC=1: P unicast stores through the peers' addresses instead of one multicast store
+  static const bool uc = [] {
+    const char* e = getenv("POS_PACK_UC");
+    return e && e[0] == '1';
+  }();
+  const int grid = pack_grid(M, N, K, dtype);
+  cudaError_t e;
+  if (flag_mode) {
+    e = uc ? launch_pack<true, false>(grid, s, in_dtype, dtype, a, no_xg(c))
+           : launch_pack<true, true>(grid, s, in_dtype, dtype, a, no_xg(c));
+  } else {
+    e = launch_pack<false, true>(grid, s, in_dtype, dtype, a, make_xg(c, kSitePackEntry));
+  }
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack_x_kernel launch");
   *done = true;
   return POS_OK;
 }
 
-int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate,
+int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate, int P,
                        cudaStream_t s) {
   clear_stale_launch_error();
-  wait_flags_kernel<<<1, 32, 0, s>>>(flags, fstate, c->world);
+  wait_flags_kernel<<<1, 32, 0, s>>>(flags, fstate, P, c->timeout_ns, c->err_dev);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "wait_flags_kernel launch");
   return POS_OK;
@@ -509,6 +689,23 @@ int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate
 }  // namespace pos
 
 using namespace pos;
+
+// ----------------------------------------------------------------- single-GPU loopback ----
+// P simulated ranks on one GPU, each with its own replica of the buffers; the P > 1 kernels above
+// run for rank 0, 1, .., P-1 in stream order with pointer tables of the local replicas.
+struct pos_loop_fc {
+  pos_ctx* c = nullptr;
+  int64_t M = 0, N = 0, K = 0;
+  int32_t dtype = POS_DT_BF16;
+  bool flag_mode = false;
+  size_t slot_bytes = 0, buf_bytes = 0;   // one gather buffer = P slots
+  std::vector<char*> buf;                 // per replica: [buffer 0 | buffer 1 | P flags] (flag mode)
+  std::vector<unsigned*> gstate;          // per replica: gather state (2 x u32)
+  std::vector<unsigned*> counter;         // per replica: dynamic tile scheduler state
+  std::vector<SfbTcPlan> plan;
+  std::vector<char> has_plan;
+  std::vector<float*> W, b;
+};
 
 extern "C" {
 
@@ -520,16 +717,12 @@ int pos_mem_alloc(pos_ctx* c, int64_t bytes, void** out) {
   void* p = nullptr;
   ncclResult_t r = ncclMemAlloc(&p, (size_t)bytes);
   if (r != ncclSuccess) return ctx_nccl_fail(c, r, "ncclMemAlloc");
-  ncclWindow_t win;
-  r = ncclCommWindowRegister(c->comm, p, (size_t)bytes, &win, NCCL_WIN_COLL_SYMMETRIC);
-  if (r != ncclSuccess) {
+  SymmWindow w;
+  if ((rc = register_window(c, state(c), p, (size_t)bytes, &w)) != POS_OK) {
     ncclMemFree(p);
-    return ctx_nccl_fail(c, r, "ncclCommWindowRegister");
+    return rc;
   }
-  state(c)->windows.push_back({static_cast<char*>(p), (size_t)bytes, win});
-  // NCCL's allocation/registration may leave a benign runtime error behind: consume it so it is
-  // not misreported by the next kernel-launch check
-  (void)cudaGetLastError();
+  state(c)->windows.push_back(w);
   cudaError_t e = cudaMemset(p, 0, (size_t)bytes);
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "cudaMemset(symmetric buffer)");
   e = cudaDeviceSynchronize();
@@ -555,9 +748,163 @@ int pos_mem_free(pos_ctx* c, void* p) {
 }
 
 int pos_mem_is_symmetric(pos_ctx* c, const void* p, int64_t bytes) {
-  ncclWindow_t w;
-  size_t off;
-  return (c && symm_lookup(c, p, (size_t)bytes, &w, &off)) ? 1 : 0;
+  return (c && symm_lookup(c, p, (size_t)bytes)) ? 1 : 0;
+}
+
+int pos_loop_sync_layer_ps(pos_ctx* c, int64_t n, float* const* grads, float* const* W,
+                           float alpha, void* stream) {
+  clear_error();
+  POS_CHECK_ARG(c && c->local, "pos_loop_* needs a context from pos_init_local");
+  POS_CHECK_ARG(n >= 1 && grads && W, "bad arguments");
+  const int P = c->world;
+  POS_CHECK_ARG(P <= kMaxPeers, "at most %d loopback ranks", kMaxPeers);
+  for (int p = 0; p < P; ++p)
+    POS_CHECK_ARG(grads[p] && W[p] && aligned16(grads[p]) && aligned16(W[p]),
+                  "rank %d: grad and W must be non-NULL and 16-byte aligned", p);
+  int rc = ctx_check(c);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  PsArgs a{};
+  for (int p = 0; p < P; ++p) {
+    a.g[p] = grads[p];
+    a.w[p] = W[p];
+  }
+  a.P = P;
+  a.alpha = alpha;
+  const int grid = ps_grid(c, n, P);
+  for (int r = 0; r < P; ++r) {   // every rank's fused reduce + apply + broadcast of its shard
+    pos_shard_range(n, P, r, &a.lo, &a.hi);
+    a.wl = W[r];
+    cudaError_t e = launch_ps<false, false>(grid, s, a, no_xg(c));
+    if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_sync_kernel launch (loopback)");
+  }
+  return POS_OK;
+}
+
+int pos_loop_fc_create(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t dtype,
+                       float* const* W, float* const* b, pos_loop_fc** out) {
+  clear_error();
+  POS_CHECK_ARG(c && c->local && out, "pos_loop_* needs a context from pos_init_local");
+  POS_CHECK_ARG(M >= 1 && N >= 1 && K >= 1 && M <= (1LL << 31) && N <= (1LL << 31), "bad M, N, K");
+  POS_CHECK_ARG(dtype == POS_DT_BF16 || dtype == POS_DT_TF32 || dtype == POS_DT_F32, "bad dtype");
+  const int P = c->world;
+  POS_CHECK_ARG(P <= kMaxPeers, "at most %d loopback ranks", kMaxPeers);
+  POS_CHECK_ARG(W, "NULL W table");
+  const bool fm = gather_flag_mode(dtype, N);
+  for (int p = 0; p < P; ++p) {
+    POS_CHECK_ARG(W[p], "rank %d: NULL W", p);
+    POS_CHECK_ARG(!fm || aligned16(W[p]), "rank %d: W must be 16-byte aligned", p);
+  }
+  pos_loop_fc* lf = new pos_loop_fc();
+  lf->c = c;
+  lf->M = M; lf->N = N; lf->K = K;
+  lf->dtype = dtype;
+  lf->flag_mode = fm;
+  lf->slot_bytes = (size_t)(K * row_elems(M, N) * dtype_bytes(dtype));
+  lf->buf_bytes = (lf->slot_bytes * P + 255) & ~size_t(255);
+  const size_t alloc = fm ? 2 * lf->buf_bytes + 256 : lf->buf_bytes;
+  lf->buf.assign(P, nullptr);
+  lf->gstate.assign(P, nullptr);
+  lf->counter.assign(P, nullptr);
+  lf->plan.resize(P);
+  lf->has_plan.assign(P, 0);
+  lf->W.assign(W, W + P);
+  lf->b.assign(P, nullptr);
+  if (b)
+    for (int p = 0; p < P; ++p) lf->b[p] = b[p];
+  int rc = POS_OK;
+  for (int p = 0; p < P && rc == POS_OK; ++p) {
+    if (cudaMalloc(&lf->buf[p], alloc) != cudaSuccess ||
+        cudaMemset(lf->buf[p], 0, alloc) != cudaSuccess ||
+        cudaMalloc(&lf->gstate[p], 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(lf->gstate[p], 0, 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMalloc(&lf->counter[p], 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(lf->counter[p], 0, 2 * sizeof(unsigned)) != cudaSuccess) {
+      (void)cudaGetLastError();
+      rc = POS_ENOMEM;
+      set_error("loopback buffers: cudaMalloc failed");
+      break;
+    }
+    if (fm) {
+      SfbTcPlan& pl = lf->plan[p];
+      lf->has_plan[p] = sfb_tc_make_plan(&pl, M, N, K * P, dtype, lf->buf[p], W[p], N,
+                                         c->max_ctas, lf->b[p], lf->buf[p] + lf->buf_bytes);
+      if (!lf->has_plan[p]) {
+        rc = POS_EUNSUPPORTED;
+        set_error("flag-mode gather without a tensor-core plan");
+        break;
+      }
+      pl.counter = lf->counter[p];
+      pl.gsel = lf->gstate[p];
+    }
+  }
+  if (rc != POS_OK) {
+    pos_loop_fc_destroy(lf);
+    return rc;
+  }
+  *out = lf;
+  return POS_OK;
+}
+
+int pos_loop_fc_sync(pos_loop_fc* lf, int32_t in_dtype, const void* const* u,
+                     const void* const* v, float alpha, void* stream) {
+  clear_error();
+  POS_CHECK_ARG(lf && u && v, "bad arguments");
+  POS_CHECK_ARG(in_dtype == POS_IN_BF16 || in_dtype == POS_IN_F32, "bad in_dtype");
+  pos_ctx* c = lf->c;
+  const int P = c->world;
+  for (int p = 0; p < P; ++p) POS_CHECK_ARG(u[p] && v[p], "rank %d: NULL factors", p);
+  int rc = ctx_check(c);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  // A2 + A3: every rank packs its factors into its slot of every replica's gather buffer
+  PackArgs a{};
+  a.M = lf->M; a.N = lf->N; a.Mp = m_pad(lf->M); a.R = row_elems(lf->M, lf->N); a.K = lf->K;
+  a.P = P;
+  const int grid = pack_grid(lf->M, lf->N, lf->K, lf->dtype);
+  for (int r = 0; r < P; ++r) {
+    if (c->fault == POS_FAULT_SKIP_PACK && c->fault_rank == r) continue;   // fault injection
+    a.u = u[r];
+    a.v = v[r];
+    const size_t mine = (size_t)r * lf->slot_bytes;
+    for (int p = 0; p < P; ++p) {
+      a.dst[0][p] = lf->buf[p] + mine;
+      a.dst[1][p] = lf->flag_mode ? lf->buf[p] + lf->buf_bytes + mine : a.dst[0][p];
+      a.flag[p] = lf->flag_mode
+                      ? reinterpret_cast<uint32_t*>(lf->buf[p] + 2 * lf->buf_bytes) + r
+                      : nullptr;
+    }
+    a.state = lf->gstate[r];
+    cudaError_t e = lf->flag_mode
+                        ? launch_pack<true, false>(grid, s, in_dtype, lf->dtype, a, no_xg(c))
+                        : launch_pack<false, false>(grid, s, in_dtype, lf->dtype, a, no_xg(c));
+    if (e != cudaSuccess) return ctx_cuda_fail(c, e, "pack_x_kernel launch (loopback)");
+  }
+  // A4 + A4b on every replica, each behind its own ready-flag wait
+  for (int r = 0; r < P; ++r) {
+    if (lf->flag_mode) {
+      const uint32_t* flags = reinterpret_cast<const uint32_t*>(lf->buf[r] + 2 * lf->buf_bytes);
+      if ((rc = symm_wait_gathered(c, flags, lf->gstate[r], P, s))) return rc;
+      cudaError_t e = sfb_tc_launch(lf->plan[r], alpha, 1, s);
+      if (e != cudaSuccess) return ctx_cuda_fail(c, e, "reconstruct launch (loopback)");
+    } else {
+      rc = reconstruct_apply(lf->M, lf->N, lf->K * P, lf->dtype, lf->buf[r], 1, lf->W[r], lf->N,
+                             lf->b[r], alpha, c->max_ctas, s);
+      if (rc != POS_OK) { if (c->sticky == POS_OK) c->sticky = rc; return rc; }
+    }
+  }
+  return POS_OK;
+}
+
+int pos_loop_fc_destroy(pos_loop_fc* lf) {
+  clear_error();
+  if (!lf) return POS_OK;
+  cudaDeviceSynchronize();
+  for (char* p : lf->buf) if (p) cudaFree(p);
+  for (unsigned* p : lf->gstate) if (p) cudaFree(p);
+  for (unsigned* p : lf->counter) if (p) cudaFree(p);
+  delete lf;
+  return POS_OK;
 }
 
 }  // extern "C"

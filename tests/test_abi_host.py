@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version():
-    assert pos.pos_version() == 100
+    assert pos.pos_version() == 200
 
 
 def test_choose_scheme_tiny_grid_bit_exact():

@@ -149,8 +149,8 @@ def test_tile_edges_exact_bitwise_k_p(MN, K, P, dtype):
 
 # ------------------------------------------------------- CTA-pair kernel (cta_group::2) ----
 # The pair kernel (256-row tiles, each CTA holding half of the V columns) is chosen for
-# K*P >= 256; POS_SFB_PAIR=1 / 0 forces it on / off at plan time so that both kernels are
-# checked on the same ragged shapes.
+# K*P >= 1024 (sfb_tc.cu POS_SFB_PAIR_KP); POS_SFB_PAIR=1 / 0 forces it on / off at plan time so that
+# both kernels are checked on the same ragged shapes.
 PAIR_MN = [(1, 4), (65, 129), (129, 260), (255, 132), (257, 1028), (1000, 4100), (4097, 64)]
 
 
@@ -189,23 +189,15 @@ def test_full_size_layers_exact_bitwise(layer):
     assert np.array_equal(bg, br)
 
 
-def test_alexnet_kp1024_sampled_rows():
-    """C1 AlexNet fc6 4096 x 9216 at K = 128, P = 8 (K*P = 1024): statistical regime, oracle on a
-    sample of rows computed one by one."""
+def test_alexnet_kp1024_full():
+    """C1 AlexNet fc6 4096 x 9216 at K = 128, P = 8 (K*P = 1024, the CTA-pair kernel): statistical
+    regime, EVERY element compared with the fp64 oracle (W' and dW), and the exact regime bitwise."""
     M, N, K, P = 4096, 9216, 128, 8
-    Us, Vs = factors(21, P, K, M, N, "stat", "bf16")
-    W = si.stat_weights(si.rng(21, 2), M, N)
-    a = -0.01 / P
-    Wd = to_dev(W)
-    ctx(P).sim_sync_layer_sfb([to_dev(u, "bf16") for u in Us], [to_dev(v, "bf16") for v in Vs], Wd, None, a, "bf16")
-    torch.cuda.synchronize()
-    rows = np.random.default_rng(0).choice(M, 64, replace=False)
-    U = np.concatenate(Us).astype(np.float64)
-    V = np.concatenate(Vs).astype(np.float64)
-    ref = W[rows].astype(np.float64) + a * (U[:, rows].T @ V)
-    got = to_host(Wd)[rows]
-    assert err(got, ref) <= TOL["bf16"]
-    assert err(got - W[rows], ref - W[rows]) <= TOL["bf16"]
+    W, _, Wg, _, Wr, _ = run_sfb(P, K, M, N, "bf16", "bf16", "stat", seed=21, bias=False)
+    assert err(Wg, Wr) <= TOL["bf16"]
+    assert err(Wg - W, Wr - W) <= TOL["bf16"]
+    _, _, Wg, bg, Wr, br = run_sfb(P, K, M, N, "bf16", "bf16", "exact", seed=22)
+    assert np.array_equal(Wg, Wr) and np.array_equal(bg, br)
 
 
 # ------------------------------------------------------------------------ degenerate cases ----

@@ -379,3 +379,82 @@ def test_sched_wait_layer_raw_gate_per_layer():
     assert still_running, "the gate waited for the whole iteration, not for layer 1 only"
     sch.close()
     ctx.close()
+
+
+def test_factors_ready_rows_must_equal_registered_k():
+    """Boundary memory safety: a trigger with fewer (or more) factor rows than the registered K is
+    refused with POS_EINVAL instead of letting the pack read past u and v."""
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, 1)
+    M, N, K = 256, 512, 16
+    W = torch.zeros(M, N, device="cuda")
+    sch.add_fc(0, M, N, K, W, None, None, "bf16", pos.POS_IN_BF16)
+    u = torch.zeros(K, M, device="cuda", dtype=torch.bfloat16)
+    v = torch.zeros(K, N, device="cuda", dtype=torch.bfloat16)
+    sch.begin(1.0)
+    for rows in (K - 1, K + 1):
+        with pytest.raises(pos.PoseidonError) as e:
+            sch.factors_ready(0, u[:rows] if rows < K else torch.zeros(rows, M, device="cuda", dtype=torch.bfloat16), v)
+        assert e.value.code == pos.POS_EINVAL
+    sch.factors_ready(0, u, v)
+    sch.end()
+    torch.cuda.synchronize()
+    sch.close()
+    ctx.close()
+
+
+def test_split_events_pack_before_weights_free():
+    """factors_ready / weights_free as separate events (§8(b)): the trigger's weights_free event is
+    recorded after a slow grad_input GEMM that reads W; the reconstruction must wait for it (the GEMM
+    sees the OLD W) while the result still equals the oracle."""
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, 1, timing=True)
+    M, N, K = 4096, 4096, 32
+    a = si.EXACT_ALPHA
+    g = si.rng(71)
+    u, v = si.exact_factors(g, K, M, N)
+    W0, b0 = si.exact_weights(g, M, N), si.exact_weights(g, M)
+    Wd, bd = to_dev(W0), to_dev(b0)
+    sch.add_fc(0, M, N, K, Wd, bd, None, "bf16", pos.POS_IN_BF16)
+    ud, vd = to_dev(u, "bf16"), to_dev(v, "bf16")
+    producer = torch.cuda.Stream()
+    producer.wait_stream(torch.cuda.current_stream())
+    ev_f, ev_w = torch.cuda.Event(), torch.cuda.Event()
+    sch.begin(a)
+    with torch.cuda.stream(producer):
+        ev_f.record(producer)
+        torch.cuda._sleep(50_000_000)                 # a slow b^l ...
+        gi = ud.float() @ Wd                          # ... whose grad_input GEMM reads W
+        ev_w.record(producer)
+        sch.factors_ready(0, ud, vd, factors_ev=ev_f, weights_free=ev_w)
+    sch.end(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    Wr, br = sync.sfb_update(W0, b0, [u], [v], a)
+    assert np.array_equal(to_host(Wd), Wr) and np.array_equal(to_host(bd), br)
+    assert np.array_equal(gi.cpu().numpy().astype(np.float64), u.astype(np.float64) @ W0.astype(np.float64))
+    sch.close()
+    ctx.close()
+
+
+def test_sched_wait_host_timeout():
+    """pos_sched_wait: a host-side bound on Alg. 2 L8 — POS_ETIMEOUT while a (slow) producer holds
+    the iteration back, then success once it completes."""
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, 1)
+    n = 4096
+    W = torch.zeros(pos.pos_padded_size(n, 1), device="cuda")
+    G = torch.ones_like(W)
+    sch.add_dense(0, n, W, G)
+    producer = torch.cuda.Stream()
+    sch.begin(1.0)
+    with torch.cuda.stream(producer):
+        torch.cuda._sleep(500_000_000)                # ~0.25 s
+        sch.grad_ready(0, producer)
+    sch.end(torch.cuda.current_stream())
+    with pytest.raises(pos.PoseidonError) as e:
+        sch.wait(5)
+    assert e.value.code == pos.POS_ETIMEOUT
+    sch.wait(0)                                       # unbounded: completes
+    assert float(W[0]) == 1.0
+    sch.close()
+    ctx.close()

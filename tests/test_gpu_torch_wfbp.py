@@ -56,3 +56,62 @@ def test_wfbp_step_equals_torch_sgd(sequential, bucket_mb):
     assert float(loss3) < float(loss2) + 1e-3
     wf.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("per_layer_gate", [False, True])
+def test_wfbp_fc_forced_to_ps_and_per_layer_gate(per_layer_gate):
+    """One FC layer synchronised by PS (flat [W|b] buffer; Algorithm 1 would pick SFB here — the
+    GoogLeNet-at-16-nodes case of PAPER:517 forced), and the per-layer forward gate of PAPER:158
+    instead of the global end: three steps equal three plain PyTorch SGD steps."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    K, lr = 16, 0.05
+    xs = [torch.randn(K, 3, 8, 8, device="cuda") for _ in range(3)]
+    ys = [torch.randint(0, 10, (K,), device="cuda") for _ in range(3)]
+    ref = make_model(1)
+    for x, y in zip(xs, ys):
+        ref.zero_grad()
+        nn.functional.cross_entropy(ref(x), y).backward()
+        with torch.no_grad():
+            for p in ref.parameters():
+                p -= lr * p.grad
+    model = make_model(1)
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    wf = Wfbp(model, ctx, K, dtype="f32", factor_dtype=torch.float32, force_ps=("6",),
+              per_layer_gate=per_layer_gate)
+    assert wf.schemes == {"6": pos.POS_SCHEME_PS, "8": pos.POS_SCHEME_SFB}
+    for x, y in zip(xs, ys):
+        wf.step(nn.functional.cross_entropy(model(x), y), lr=lr)
+    torch.cuda.synchronize()
+    for (n, p), (_, q) in zip(model.named_parameters(), ref.named_parameters()):
+        got, exp = p.detach().double().cpu().numpy(), q.detach().double().cpu().numpy()
+        assert np.max(np.abs(got - exp)) <= 1e-5 * np.max(np.abs(exp)), n
+    wf.close()
+    ctx.close()
+
+
+def test_wfbp_short_last_batch_is_padded_and_long_batch_raises():
+    """A short last batch (K' < K rows) is padded with zero factor rows (they add nothing to U^T V):
+    the step equals torch SGD on the K' samples; more rows than K is refused."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    K, Ks, lr = 16, 11, 0.05
+    x = torch.randn(Ks, 3, 8, 8, device="cuda")
+    y = torch.randint(0, 10, (Ks,), device="cuda")
+    ref = make_model(2)
+    nn.functional.cross_entropy(ref(x), y).backward()
+    with torch.no_grad():
+        expect = {n: (p - lr * p.grad).detach().clone() for n, p in ref.named_parameters()}
+    model = make_model(2)
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    wf = Wfbp(model, ctx, K, dtype="f32", factor_dtype=torch.float32)
+    wf.step(nn.functional.cross_entropy(model(x), y), lr=lr)
+    torch.cuda.synchronize()
+    for n, p in model.named_parameters():
+        got, exp = p.detach().double().cpu().numpy(), expect[n].double().cpu().numpy()
+        assert np.max(np.abs(got - exp)) <= 1e-5 * np.max(np.abs(exp)), n
+    xl = torch.randn(K + 1, 3, 8, 8, device="cuda")
+    with pytest.raises(ValueError):
+        wf.step(nn.functional.cross_entropy(model(xl), torch.zeros(K + 1, dtype=torch.long, device="cuda")), lr=lr)
+    wf.close()
+    ctx.close()
