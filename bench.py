@@ -43,6 +43,23 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 NVLINK_GBS_PER_DIR = 770.0   # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
+def load_nvlink(P):
+    """Achievable per-direction NVLink bandwidth for P GPUs, measured by scripts/nvlink_peaks.py
+    (nccl-tests style AG / RS busbw, profiles/nvlink_peaks.json); else the guide's peer-copy
+    figure."""
+    p = os.path.join(ROOT, "profiles", "nvlink_peaks.json")
+    if P > 1 and os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        key = f"P{P}"
+        if key in d:
+            return float(d[key]["per_dir_gbs"]), f"measured (profiles/nvlink_peaks.json {key}: max NCCL AG/RS busbw)"
+        near = sorted(d, key=lambda k: abs(int(k[1:]) - P))
+        if near:
+            return float(d[near[0]]["per_dir_gbs"]), f"measured at {near[0]} (profiles/nvlink_peaks.json; no {key} entry)"
+    return NVLINK_GBS_PER_DIR, "B200_PROFILING.md peer-copy figure (770 GB/s per direction)"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -69,6 +86,9 @@ def parse():
                          "2 MB KV pairs); 0 = one unit per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tf32", action="store_true", help="skip the extra tf32-factor measurement")
+    ap.add_argument("--no-trace", action="store_true",
+                    help="time the apply kernels with CUDA events (graph nodes) instead of device-side tracing")
     ap.add_argument("--no-symm", action="store_true",
                     help="P > 1: keep PS buffers and SFB gather buffers out of symmetric (NVLS) memory, i.e. use the stock NCCL collectives")
     ap.add_argument("--static-tiles", action="store_true", help="static round-robin reconstruction tiles")
@@ -142,10 +162,10 @@ def _shard_len(n, P):
     return hi - lo
 
 
-def roofline_times(rows, peaks, P):
+def roofline_times(rows, peaks, P, nvl_gbs=NVLINK_GBS_PER_DIR):
     hbm = peaks["hbm_gbs"] * 1e9
     tc = peaks["bf16_tflops"] * 1e12
-    nvl = NVLINK_GBS_PER_DIR * 1e9
+    nvl = nvl_gbs * 1e9
     t_nvl = sum(r["nvl"] for r in rows) / nvl if P > 1 else 0.0
     t_k = sum(max(r["flop_a4"] / tc, (r["hbm_a4"] + r["hbm_other"]) / hbm) for r in rows)
     t_seq = sum((r["nvl"] / nvl if P > 1 else 0.0) + max(r["flop_a4"] / tc, (r["hbm_a4"] + r["hbm_other"]) / hbm)
@@ -241,6 +261,72 @@ def make_step(sch, bufs, alpha):
                 sch.grad_ready(l, stream)
         sch.end(stream)
     return step
+
+
+def isolated_kernels(pos, model, units, K, P, dtype, peaks):
+    """Each hot-path kernel ALONE: back-to-back launches through the C ABI between
+    two CUDA events on the launching stream, inputs larger than L2 rotated between launches;
+    algorithmic bytes (flops) per launch / average launch time, against the measured peak.
+      A4  reconstruct-and-apply, the model's largest SFB layer at K*P rows: 8MN + s(M+N)KP bytes
+      A7  PS shard apply over the model's largest dense unit's shard: 12 bytes per element
+      A2  factor pack of the largest SFB layer: K(M+N)(in + out) bytes."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = {"bf16": pos.POS_DT_BF16, "tf32": pos.POS_DT_TF32, "f32": pos.POS_DT_F32}[dtype]
+    eb = 2 if dtype == "bf16" else 4
+    fdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    hbm = peaks["hbm_gbs"]
+    out = {}
+
+    def timed(fn, n_launch=20, rot=2):
+        for i in range(3):
+            fn(i % rot)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(n_launch):
+            fn(i % rot)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n_launch
+
+    fcs = [model.layers[u["layers"][0]] for u in units if u["kind"] == "fc"]
+    if fcs:
+        ly = max(fcs, key=lambda l: l.M * l.N)
+        M, N, KP = ly.M, ly.N, K * P
+        R = pos.pos_factor_row_elems(M, N)
+        G = (torch.randn(KP, R, device=dev) * 0.03).to(fdt)
+        Ws = [torch.randn(M, N, device=dev) for _ in range(2)]
+        b = torch.zeros(M, device=dev)
+        ms = timed(lambda i: pos.pos_reconstruct_apply(M, N, KP, dt, G, Ws[i], b, -1e-3))
+        byts = 8 * M * N + eb * KP * (M + N)
+        out["a4_reconstruct_apply"] = {
+            "layer": f"{ly.name} {M}x{N}, K*P={KP}", "us": ms * 1e3, "achieved_gbs": byts / ms / 1e6,
+            "frac_hbm": byts / ms / 1e6 / hbm, "tflops": 2 * M * N * KP / ms / 1e9,
+            "frac_bf16_peak": 2 * M * N * KP / ms / 1e9 / peaks["bf16_tflops"]}
+        u = torch.randn(K, M, device=dev).to(fdt)
+        v = torch.randn(K, N, device=dev).to(fdt)
+        slots = [torch.empty(K * R, device=dev, dtype=fdt) for _ in range(2)]
+        ms = timed(lambda i: pos.pos_pack_factors(u, v, slots[i], dt), n_launch=50)
+        byts = K * (M + N) * (eb + eb)
+        out["a2_pack"] = {"layer": f"{ly.name} K={K}", "us": ms * 1e3, "achieved_gbs": byts / ms / 1e6,
+                          "frac_hbm": byts / ms / 1e6 / hbm,
+                          "note": "a few MB per launch: launch/latency-bound, not bandwidth-bound"}
+        del G, Ws, slots
+    dens = [u for u in units if u["kind"] == "dense"]
+    if dens:
+        n = max(u["n"] for u in dens)
+        lo, hi = pos.pos_shard_range(n, P, 0)
+        cnt = max(hi - lo, 1)
+        n_rot = max(2, int(math.ceil(3 * 126e6 / (8 * cnt))))    # rotate > 3x L2 of W + g
+        gs = [torch.randn(cnt, device=dev) for _ in range(n_rot)]
+        Wx = [torch.randn(cnt, device=dev) for _ in range(n_rot)]
+        ms = timed(lambda i: pos.pos_ps_apply(gs[i], Wx[i], cnt, -1e-3), rot=n_rot)
+        out["a7_ps_apply"] = {"elements": cnt, "us": ms * 1e3, "achieved_gbs": 12 * cnt / ms / 1e6,
+                              "frac_hbm": 12 * cnt / ms / 1e6 / hbm,
+                              "note": "shard of the largest dense unit; the fused NVLS kernel (P > 1) "
+                                      "moves its reduce / broadcast over NVLink instead"}
+    return out
 
 
 def capture_ring(fn, main, n=4):
@@ -356,7 +442,10 @@ def run_ours(a):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * 1 + rank)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
-    sch = pos.Scheduler(ctx, L, timing=("apply" if not a.layers else True), sequential=a.sequential,
+    # in-step kernel times come from device-side tracing (the kernels stamp %globaltimer): no
+    # timing events in the captured step; --layers adds per-stage events and a timeline
+    sch = pos.Scheduler(ctx, L, timing=(True if a.layers else ("apply" if a.no_trace else False)),
+                        trace=not a.no_trace, sequential=a.sequential,
                         symm=not a.no_symm, ps_after_sfb=a.ps_after_sfb, static_tiles=a.static_tiles)
     bufs = register_units(pos, ctx, sch, model, units, K, a.dtype, device_fill(gen, a.dtype),
                           symm=not a.no_symm)
@@ -391,35 +480,52 @@ def run_ours(a):
     _log("graph warmup done")
     refresh_grads()      # reduce-scatter sums in place; start the timed region from fresh gradients
     torch.cuda.synchronize()
-    sch.timing_reset()
+    if a.layers or a.no_trace:
+        sch.timing_reset()
+    if not a.no_trace:
+        sch.trace_reset()
 
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
     t_wall0 = time.time()
-    e0.record(main)
+    evs[0].record(main)
     h0 = time.perf_counter()
     for i in range(a.steps):
         run(i)
+        evs[i + 1].record(main)
     host_ms = (time.perf_counter() - h0) * 1e3 / a.steps   # host enqueue cost per step
-    e1.record(main)
     torch.cuda.synchronize()
     barrier()
     t_wall1 = time.time()
-    ms = e0.elapsed_time(e1) / a.steps
+    ms = evs[0].elapsed_time(evs[-1]) / a.steps
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(a.steps)]
     _log(f"timed region done: {ms:.4f} ms/step")
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        t = torch.tensor([ms] + per_step, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)          # max over ranks (per step)
+        ms, per_step = float(t[0].item()), [float(x) for x in t[1:].tolist()]
+    ps_sorted = sorted(per_step)
+    step_stats = {"median_ms": statistics.median(per_step),
+                  "p90_ms": ps_sorted[min(len(ps_sorted) - 1, int(math.ceil(0.9 * len(ps_sorted))) - 1)],
+                  "min_ms": ps_sorted[0], "max_ms": ps_sorted[-1],
+                  "note": "per-step device time (CUDA events between consecutive steps), max over ranks per step"}
     # span of the reconstructions within the step (they overlap: two streams) — before timing(),
     # which retires the events in eager mode
-    a4_span_ms = sch.timing_span(pos.POS_SCHEME_SFB) if any(
-        u["kind"] == "fc" for u in units) else None
-    unit_times = [sch.timing(un["layers"][0]) for un in units]
+    has_fc, has_dense = any(u["kind"] == "fc" for u in units), any(u["kind"] == "dense" for u in units)
+    if a.no_trace:    # CUDA-event timing of the apply stages (events inside the captured step)
+        a4_span_ms = sch.timing_span(pos.POS_SCHEME_SFB) if has_fc else None
+        ps_span_ms = sch.timing_span(pos.POS_SCHEME_PS) if has_dense else None
+    else:
+        a4_span_ms = sch.trace_span(pos.POS_SCHEME_SFB)[0] / 1e3 if has_fc else None
+        ps_span_ms = sch.trace_span(pos.POS_SCHEME_PS)[0] / 1e3 if has_dense else None
+    timeline = sch.timeline(len(units)) if a.layers else None
+    unit_apply_ms = [(sch.timing(un["layers"][0])[2] if a.no_trace else sch.trace(un["layers"][0])[0] / 1e3)
+                     for un in units]
+    unit_times = [sch.timing(un["layers"][0]) for un in units] if a.layers else None
     # clock soak: if the timed region was too short for the 50 ms sampler, keep the same load
     # running (untimed) for ~1 s so the clock record describes this workload under load
     soak_t0 = soak_t1 = None
@@ -503,8 +609,58 @@ def run_ours(a):
         e2e = {"value": P * model.total_params / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "note": "per step: H2D of every layer's factors/gradients from pinned host memory, each layer "
-                       "triggered after its upload (backward order), D2H of the FC biases"
+                       "triggered after its upload (backward order), D2H of the FC biases (the "
+                       "step's only host-visible result: W stays device-resident, as in training)"
                        + ("" if a.eager else "; step captured as a CUDA graph")}
+    # ---- the same step with tf32 factors (4-byte floats, the paper's element width) ----
+    tf32 = None
+    if a.dtype == "bf16" and not a.no_tf32:
+        sch2 = pos.Scheduler(ctx, L, trace=True, symm=not a.no_symm)
+        bufs2 = []
+        for l, bb in enumerate(bufs):
+            if bb["kind"] == "fc":
+                b2 = dict(bb, u=bb["u"].float(), v=bb["v"].float())
+                ly = model.layers[l]
+                sch2.add_fc(l, ly.M, ly.N, K, bb["W"], bb["b"], None, dtype="tf32", in_dtype=pos.POS_IN_F32)
+                bufs2.append(b2)
+            else:
+                bufs2.append(bb)
+        for un in units:
+            if un["kind"] == "dense":
+                bb = bufs[un["layers"][0]]
+                sch2.add_dense_bucket(un["layers"][0], un["sizes"], bb["Wflat"], bb["gflat"])
+        step2 = make_step(sch2, bufs2, alpha)
+        for _ in range(3):
+            step2(main)
+        g2 = capture_ring(step2, main)
+        for i in range(len(g2)):
+            g2[i].replay()
+        refresh_grads()
+        torch.cuda.synchronize()
+        sch2.trace_reset()
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(main)
+        for i in range(a.steps):
+            g2[i % len(g2)].replay()
+        q1.record(main)
+        torch.cuda.synchronize()
+        ms2 = q0.elapsed_time(q1) / a.steps
+        span2 = sch2.trace_span(pos.POS_SCHEME_SFB)[0] / 1e3
+        if world > 1:
+            t = torch.tensor([ms2, span2], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms2, span2 = (float(x) for x in t.tolist())
+        rows2 = unit_accounting(model, units, K, P, "tf32")
+        b2_a4 = sum(r["hbm_a4"] for r in rows2)
+        tf32 = {"ms_per_step": ms2, "value": P * model.total_params / (ms2 / 1e3), "unit": UNIT,
+                "a4_span_ms": span2, "a4_achieved_gbs": b2_a4 / (span2 / 1e3) / 1e9,
+                "a4_frac_hbm": b2_a4 / (span2 / 1e3) / 1e9 / load_peaks()["hbm_gbs"],
+                "note": "factors gathered as fp32 and contracted with tcgen05 kind::tf32 (fp32 accumulate)"}
+        g2 = None
+        torch.cuda.synchronize()
+        sch2.close()
+    kern_iso = isolated_kernels(pos, model, units, K, P, a.dtype, load_peaks())
     clocks.stop()
     if soak_t0 is not None:
         clk = clocks.summary(soak_t0, soak_t1)
@@ -516,13 +672,14 @@ def run_ours(a):
     # ---- accounting & roofline ----
     peaks = load_peaks()
     rows = unit_accounting(model, units, K, P, a.dtype)
-    t_pipe, t_seq, t_nvl, t_kern = roofline_times(rows, peaks, P)
+    nvl_gbs, nvl_src = load_nvlink(P)
+    t_pipe, t_seq, t_nvl, t_kern = roofline_times(rows, peaks, P, nvl_gbs)
     a4_bytes = sum(r["hbm_a4"] for r in rows)
     a4_flop = sum(r["flop_a4"] for r in rows)
-    a4_ms_sum = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "SFB")
+    a4_ms_sum = sum(unit_apply_ms[i] for i, r in enumerate(rows) if r["scheme"] == "SFB")
     a4_ms = a4_span_ms if a4_span_ms else a4_ms_sum
     ps_bytes = sum(r["hbm_other"] for r in rows if r["scheme"] == "PS")
-    ps_ms = sum(unit_times[i][2] for i, r in enumerate(rows) if r["scheme"] == "PS")
+    ps_ms = sum(unit_apply_ms[i] for i, r in enumerate(rows) if r["scheme"] == "PS")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -537,18 +694,26 @@ def run_ours(a):
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic,
             "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
-            "kernel_ms_note": "span from the first reconstruction's start to the last one's end in "
-                              "a step (consecutive layers' reconstructions overlap on two streams); "
-                              "sum of per-layer durations: %.4f ms" % a4_ms_sum,
+            "kernel_ms_note": "device-side trace (%%globaltimer stamped by the kernels, no events in "
+                              "the captured step), averaged over the timed steps: span from the first "
+                              "reconstruction CTA's start to the last one's end in a step (consecutive "
+                              "layers' reconstructions overlap on two streams); sum of per-layer "
+                              "durations: %.4f ms" % a4_ms_sum,
+            "per_layer_ms": {model.layers[un["layers"][0]].name: unit_apply_ms[i]
+                             for i, un in enumerate(units) if un["kind"] == "fc"},
             "peak_source": peaks["source"],
             "tensor_tflops": a4_flop / (a4_ms / 1e3) / 1e12 if a4_ms > 0 else None,
             "tensor_frac_of_bf16_peak": (a4_flop / (a4_ms / 1e3) / 1e12) / peaks["bf16_tflops"] if a4_ms > 0 else None,
-            "ps_apply": {"achieved_gbs": ps_bytes / (ps_ms / 1e3) / 1e9 if ps_ms > 0 else None,
-                         "frac": (ps_bytes / (ps_ms / 1e3) / 1e9) / peaks["hbm_gbs"] if ps_ms > 0 else None,
-                         "algorithmic_bytes_per_step": ps_bytes, "kernel_ms_per_step": ps_ms},
+            "ps_units_in_step": {"algorithmic_bytes_per_step": ps_bytes, "sum_of_unit_ms": ps_ms,
+                                 "span_ms": ps_span_ms,
+                                 "note": "PS units run concurrently with the reconstructions and with "
+                                         "each other: their summed durations are not a kernel time; "
+                                         "see kernels_isolated.a7_ps_apply"},
+            "kernels_isolated": kern_iso,
             "step": {"t_roofline_pipelined_ms": t_pipe * 1e3, "t_roofline_sequential_ms": t_seq * 1e3,
                      "t_nvlink_ms": t_nvl * 1e3, "t_kernels_ms": t_kern * 1e3,
-                     "frac_pipelined": (t_pipe * 1e3) / ms, "nvlink_gbs_per_dir": NVLINK_GBS_PER_DIR}}
+                     "frac_pipelined": (t_pipe * 1e3) / ms, "nvlink_gbs_per_dir": nvl_gbs,
+                     "nvlink_source": nvl_src}}
     symm_on = P > 1 and not a.no_symm
     flags_on = symm_on and os.environ.get("POS_GATHER_FLAGS", "1") != "0" and a.dtype != "f32"
     n_launch = 0
@@ -570,7 +735,7 @@ def run_ours(a):
         if ly.kind != "fc":
             continue
         s_b, t_s, t_p = pos.pos_scheme_times_b200(ly.M, ly.N, K, P, 2 if a.dtype == "bf16" else 4,
-                                                  peaks["hbm_gbs"] * 1e9, NVLINK_GBS_PER_DIR * 1e9,
+                                                  peaks["hbm_gbs"] * 1e9, nvl_gbs * 1e9,
                                                   peaks["bf16_tflops"] * 1e12)
         choice.append({"layer": ly.name, "alg1": pos.SCHEME_NAMES[pos.pos_choose_scheme(ly.M, ly.N, K, P)],
                        "b200_model": pos.SCHEME_NAMES[s_b], "t_sfb_us": t_s * 1e6, "t_ps_us": t_p * 1e6})
@@ -595,7 +760,9 @@ def run_ours(a):
         "host_enqueue_ms_per_step": host_ms,
         "launch_mode": "eager" if a.eager else "cuda_graph (4-graph ring, one step each)",
         "eager_ms_per_step": eager_ms,
+        "step_stats": step_stats,
         "roofline": roof,
+        "tf32": tf32,
         "clocks": clk,
         "e2e": e2e,
         "scheme_choice": choice,
@@ -603,9 +770,14 @@ def run_ours(a):
         "gpu_launches_note": "libposeidon kernels per timed region (NCCL kernels and cudaMemsetAsync not counted)",
     }
     if a.layers and rank == 0:
-        for l, (r, lt) in enumerate(zip(rows, unit_times)):
-            print(f"{l:3d} {r['name']:>20s} {r['scheme']:>3s} params={r['params']:>11d} pack={lt[0]*1e3:8.1f}us "
-                  f"comm={lt[1]*1e3:8.1f}us apply={lt[2]*1e3:8.1f}us", file=sys.stderr)
+        print("unit name scheme params | mean pack/comm/apply us | timeline of the last step (us from the "
+              "first unit's start): start packed gathered apply0 apply1 done", file=sys.stderr)
+        for l, (r, lt, tl) in enumerate(zip(rows, unit_times, timeline)):
+            lt = (lt[0], lt[1], unit_apply_ms[l])
+            print(f"{l:3d} {r['name']:>20s} {r['scheme']:>3s} params={r['params']:>11d} pack={lt[0]*1e3:8.1f} "
+                  f"comm={lt[1]*1e3:8.1f} apply={lt[2]*1e3:8.1f} | " +
+                  " ".join(f"{x * 1e3:8.1f}" if x >= 0 else "       -" for x in tl), file=sys.stderr)
+        out["timeline_us"] = [[round(x * 1e3, 1) for x in tl] for tl in timeline]
     cpu = None
     if rank == 0 and P == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline_sample(a.config, P, a.dtype, min_seconds=10.0)
@@ -664,6 +836,17 @@ def _cores():
     return os.cpu_count()
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline_sample(config, P, dtype, min_seconds=10.0):
     sample, params, desc = _oracle_sample(config, P, dtype)
     _oracle_step(sample, -0.01 / P)      # warm
@@ -676,7 +859,8 @@ def cpu_baseline_sample(config, P, dtype, min_seconds=10.0):
             break
     dt = (time.perf_counter() - t0) / n
     return {"value": P * params / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
-            "sample": desc + f"; {n} repetitions, {dt * 1e3:.1f} ms each", "os_cpu_count": os.cpu_count()}
+            "sample": desc + f"; {n} repetitions, {dt * 1e3:.1f} ms each", "os_cpu_count": os.cpu_count(),
+            "cpu_model": _cpu_model()}
 
 
 def run_reference(a):
@@ -701,7 +885,8 @@ def run_reference(a):
            "config": {"workload": f"{model_name} full-model gradient sync ({a.config}), K={K}/GPU — oracle on a "
                                   "bounded sample (see cpu_baseline.sample)", "per_gpu_batch": K,
                       "global_batch": K * P, "parallelism": f"dp{P} (computed on host, rank 0)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": desc},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle", "sample": desc,
+                            "cpu_model": _cpu_model()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), file=_JSON_OUT, flush=True)
 

@@ -75,7 +75,9 @@ enum { POS_SCHED_TIMING = 1, POS_SCHED_SEQUENTIAL = 2, POS_SCHED_TIMING_APPLY = 
        POS_SCHED_PS_AFTER_SFB = 16 /* P > 1: a dense unit's sync waits for the previously issued
                                       SFB reconstruction instead of overlapping it */,
        POS_SCHED_STATIC_TILES = 32 /* reconstruction tiles in static round-robin order instead of
-                                      the dynamic (atomic-counter) tile scheduler */ };
+                                      the dynamic (atomic-counter) tile scheduler */,
+       POS_SCHED_TRACE = 64 /* device-side tracing: the apply kernels stamp %globaltimer into device
+                               records (pos_sched_trace*) — no event nodes on the streams */ };
 
 /* ABI version (major * 100 + minor): 200 = split factors_ready / weights_free trigger events, watchdog, loopback. */
 int pos_version(void);
@@ -339,6 +341,21 @@ int pos_sched_scheme(pos_sched* s, int32_t l);
  * runs it. Synchronises on the layer's outstanding iterations. Returns the iteration count (> 0). */
 int pos_sched_timing(pos_sched* s, int32_t l, float* pack_ms, float* comm_ms, float* apply_ms);
 int pos_sched_timing_reset(pos_sched* s);
+/* Tracing, POS_SCHED_TIMING only: the device timeline of the most recent iteration —
+ * for unit u (pos_sched_unit_of), out[6u .. 6u+5] = milliseconds of its [start, packed, gathered,
+ * apply start, apply end, done] events relative to the first-issued unit's start (-1 = no such
+ * stage). Writes at most max_units units; returns the number of units. */
+int pos_sched_timeline(pos_sched* s, float* out, int32_t max_units);
+/* Device-side tracing (POS_SCHED_TRACE): layer l's unit apply kernel (reconstruct-and-apply; shard
+ * apply or fused NVLS PS kernel) — average and last launch duration in microseconds (first CTA
+ * start to last CTA end, %globaltimer) and the number of launches since the last reset. Outputs may
+ * be NULL. Synchronises the device. */
+int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, int64_t* launches);
+/* The SPAN of all apply kernels of `scheme` within one step (earliest CTA start of the first to the
+ * latest CTA end of the last; they overlap on several streams), averaged over steps. POS_ESTATE if
+ * the scheme has no traced kernels (e.g. the SIMT f32 path). */
+int pos_sched_trace_span(pos_sched* s, int32_t scheme, double* avg_us, int64_t* steps);
+int pos_sched_trace_reset(pos_sched* s);
 /* With POS_SCHED_TIMING(_APPLY): the device-time SPAN (earliest apply start to latest apply end)
  * of all units of `scheme` (POS_SCHEME_SFB or POS_SCHEME_PS) within one iteration, averaged over
  * the (up to 4) most recent iterations whose timing events are still live. Reconstructions of

@@ -23,7 +23,7 @@ POS_ETIMEOUT = -7
 POS_REDUCE_SWITCH, POS_REDUCE_RANK_ORDER = 0, 1
 POS_FAULT_NONE, POS_FAULT_SKIP_PS, POS_FAULT_SKIP_PACK = 0, 1, 2
 POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY, POS_SCHED_NO_SYMM, POS_SCHED_PS_AFTER_SFB = 1, 2, 4, 8, 16
-POS_SCHED_STATIC_TILES = 32
+POS_SCHED_STATIC_TILES, POS_SCHED_TRACE = 32, 64
 
 DTYPES = {"bf16": POS_DT_BF16, "tf32": POS_DT_TF32, "f32": POS_DT_F32}
 SCHEME_NAMES = {POS_SCHEME_PS: "PS", POS_SCHEME_SFB: "SFB", POS_SCHEME_ADAM: "ADAM"}
@@ -312,14 +312,15 @@ class Scheduler:
     """pos_sched: WFBP per-layer scheduler (Algorithm 2 on CUDA streams/events)."""
 
     def __init__(self, ctx: Context, n_layers: int, timing=False, sequential=False, symm=True,
-                 ps_after_sfb=False, static_tiles=False):
+                 ps_after_sfb=False, static_tiles=False, trace=False):
         """timing: False | True (all stages) | "apply" (apply stage only). symm: place SFB gather
         buffers in symmetric memory (multicast factor pack) when world > 1."""
         self.ctx = ctx
         h = C.c_void_p()
         tflag = POS_SCHED_TIMING_APPLY if timing == "apply" else (POS_SCHED_TIMING if timing else 0)
         flags = (tflag | (POS_SCHED_SEQUENTIAL if sequential else 0) | (0 if symm else POS_SCHED_NO_SYMM)
-                 | (POS_SCHED_PS_AFTER_SFB if ps_after_sfb else 0) | (POS_SCHED_STATIC_TILES if static_tiles else 0))
+                 | (POS_SCHED_PS_AFTER_SFB if ps_after_sfb else 0) | (POS_SCHED_STATIC_TILES if static_tiles else 0)
+                 | (POS_SCHED_TRACE if trace else 0))
         _chk(lib().pos_sched_create(ctx.h, n_layers, flags, C.byref(h)), "pos_sched_create")
         self.h = h
         self.L = n_layers
@@ -387,6 +388,28 @@ class Scheduler:
         a, b, c = C.c_float(), C.c_float(), C.c_float()
         _chk(lib().pos_sched_timing(self.h, l, C.byref(a), C.byref(b), C.byref(c)), "pos_sched_timing")
         return a.value, b.value, c.value
+
+    def timeline(self, n_units):
+        """pos_sched_timeline: per unit [start, packed, gathered, apply0, apply1, done] in ms."""
+        buf = (C.c_float * (6 * n_units))()
+        n = _chk(lib().pos_sched_timeline(self.h, buf, n_units), "pos_sched_timeline")
+        return [list(buf[6 * u:6 * u + 6]) for u in range(min(n, n_units))]
+
+    def trace(self, l):
+        """pos_sched_trace: (average us, last us, launches) of layer l's unit apply kernel."""
+        a, b, n = C.c_double(), C.c_double(), C.c_int64()
+        _chk(lib().pos_sched_trace(self.h, l, C.byref(a), C.byref(b), C.byref(n)), "pos_sched_trace")
+        return a.value, b.value, n.value
+
+    def trace_span(self, scheme=None):
+        """pos_sched_trace_span: (average us, steps) of the step's apply-kernel span of `scheme`."""
+        a, n = C.c_double(), C.c_int64()
+        _chk(lib().pos_sched_trace_span(self.h, POS_SCHEME_SFB if scheme is None else scheme,
+                                        C.byref(a), C.byref(n)), "pos_sched_trace_span")
+        return a.value, n.value
+
+    def trace_reset(self):
+        _chk(lib().pos_sched_trace_reset(self.h), "pos_sched_trace_reset")
 
     def timing_reset(self):
         _chk(lib().pos_sched_timing_reset(self.h), "pos_sched_timing_reset")

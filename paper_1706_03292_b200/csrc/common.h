@@ -70,12 +70,64 @@ inline cudaError_t record_timing_event(cudaEvent_t e, cudaStream_t s) {
              : cudaEventRecord(e, s);
 }
 
+// ---- device-side launch trace (SURVEY §5 tracing) ----
+// Kernels stamp %globaltimer into a record in device memory instead of the host bracketing them
+// with CUDA events (inside a CUDA graph every event record is one more node on the critical
+// stream). An INTERVAL is `expected` CTAs: one launch (its grid) or a group of launches (the sum of
+// their grids, e.g. all reconstructions of one step). Record words (u64):
+//   [0] earliest CTA start of the interval in progress (~0 = none)   [1] latest CTA end
+//   [2] CTAs finished                                               [3] intervals completed
+//   [4] sum of interval durations (ns)                              [5], [6] last interval's start, end
+struct KTrace {
+  unsigned long long* rec = nullptr;   // nullptr = tracing off
+  unsigned expected = 0;
+};
+constexpr int kTraceWords = 8;
+// allocate / re-arm a record (host)
+cudaError_t ktrace_alloc(unsigned long long** rec);
+cudaError_t ktrace_reset(unsigned long long* rec);
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long ktrace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// thread 0 of every CTA, first thing
+__device__ __forceinline__ void ktrace_begin(const KTrace& t) {
+  if (t.rec && threadIdx.x == 0) atomicMin(t.rec, ktrace_now());
+}
+// thread 0 of every CTA, after the whole CTA's work (callers __syncthreads() first); the last CTA
+// of the interval folds it into the sums and re-arms the record
+__device__ __forceinline__ void ktrace_end(const KTrace& t) {
+  if (!t.rec || threadIdx.x != 0) return;
+  atomicMax(t.rec + 1, ktrace_now());
+  __threadfence();
+  if (atomicAdd(t.rec + 2, 1ull) == (unsigned long long)t.expected - 1) {
+    __threadfence();
+    const unsigned long long s = atomicOr(t.rec + 0, 0ull), e = atomicOr(t.rec + 1, 0ull);
+    t.rec[5] = s;
+    t.rec[6] = e;
+    t.rec[4] += e > s ? e - s : 0;
+    t.rec[3] += 1;
+    atomicExch(t.rec + 0, ~0ull);
+    atomicExch(t.rec + 1, 0ull);
+    atomicExch(t.rec + 2, 0ull);
+    __threadfence();
+  }
+}
+#endif
+
 // ---- kernel launchers (return cudaError_t of the launch) ----
 cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                                 const void* u, const void* v, void* slot, cudaStream_t s);
 cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                                int32_t accumulate, float* b, float alpha, cudaStream_t s);
-cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s);
+// tr.rec != nullptr: traced; tr.expected = 0 means "this launch alone" (set to its grid)
+cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s,
+                            KTrace tr = {}, KTrace tg = {});
+// grid of launch_ps_apply's vector kernel for `count` 16-byte-aligned elements (0 = no vector part)
+int ps_apply_grid(int64_t count);
 constexpr int kMaxSimP = 16;
 constexpr int kMaxPeers = 16;   // ranks addressable by the fused symmetric-memory kernels
 
@@ -123,6 +175,7 @@ struct SfbTcPlan {
   // scheduler; nullptr = static round-robin tiles. Launches sharing a counter must not overlap.
   unsigned int* counter = nullptr;
   float* bias = nullptr;   // fused A4b target (nullptr = no bias)
+  KTrace trace, group;     // device-side launch trace of this launch / of a group of launches
 };
 // false if the shape/alignment/dtype cannot use the tensor-core kernel
 bool sfb_tc_make_plan(SfbTcPlan* plan, int64_t M, int64_t N, int64_t KP, int32_t dtype,

@@ -56,14 +56,27 @@ int ctx_workspace(pos_ctx* c, size_t bytes, void** out) {
 }
 
 // A5 + A6 + A7 + A8 for a dense (or flattened FC) layer of n parameters, on stream s.
+int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W) {
+  const int P = c->world;
+  if (P > 1 && !c->local) {
+    const int64_t padded = pos_padded_size(n, P);
+    if (symm_lookup(c, grad, (size_t)padded * 4) && symm_lookup(c, W, (size_t)padded * 4))
+      return symm_ps_grid(c, n);
+  }
+  int64_t lo = 0, hi = n;
+  if (!c->local) pos_shard_range(n, P, c->rank, &lo, &hi);
+  return hi > lo ? ps_apply_grid(hi - lo) : 0;
+}
+
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail) {
+                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail, KTrace tr,
+                   KTrace tg) {
   const int P = c->world;
   const int64_t S = pos_shard_stride(n, P);
   if (S < 0) return (int)S;
   {  // NVLS fused kernel when grad and W live in symmetric memory (NEXT-1)
     bool done = false;
-    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done);
+    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done, tr, tg);
     if (rc != POS_OK || done) return rc;
   }
   const int64_t padded = S * P;
@@ -87,7 +100,7 @@ int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cu
     pos_shard_range(n, P, r, &lo, &hi);
   }
   if (hi > lo) {
-    cudaError_t e = launch_ps_apply(grad + lo, W + lo, hi - lo, alpha, s);
+    cudaError_t e = launch_ps_apply(grad + lo, W + lo, hi - lo, alpha, s, tr, tg);
     if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_apply launch");
   }
   if (ev_apply_done) POS_CUDA_TRY(record_timing_event(ev_apply_done, s));

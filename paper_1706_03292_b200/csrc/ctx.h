@@ -44,7 +44,10 @@ inline ncclDataType_t nccl_type(int32_t dtype) {
 // zero_tail: zero grad[n, P*S) first (the one-shot API; the scheduler zeroes it once at add time
 // and the tail stays zero because the in-place reduce-scatter only ever sums zeros into it).
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail);
+                   cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail,
+                   KTrace tr = {}, KTrace tg = {});
+// grid of the traced kernel stage_ps_dense launches for a unit of n parameters on this rank
+int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W);
 int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
                         int32_t dtype, const void* u, const void* v, void* pack_buf, float* grad,
                         int32_t has_bias, cudaStream_t s);
@@ -54,7 +57,10 @@ void symm_destroy(pos_ctx* c);
 // fused reduce-scatter + apply + all-gather over NVLS when grad and W are symmetric; *done = false
 // (and nothing enqueued) otherwise
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done);
+                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr = {},
+                  KTrace tg = {});
+// grid of the fused PS kernel for a unit of n parameters (rank-invariant)
+int symm_ps_grid(pos_ctx* c, int64_t n);
 // pack this rank's factors and multicast them into every rank's gather buffer when the gather
 // buffer is symmetric; *done = false otherwise. Barrier mode (gbuf2 == nullptr): entry + exit
 // barriers. Flag mode: gbuf / gbuf2 double buffer (by iteration parity) and the P ready flags, all

@@ -110,7 +110,9 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 }
 
 __global__ void ps_apply_vec_kernel(const float4* __restrict__ g, float4* __restrict__ W,
-                                    int64_t n4, float alpha) {
+                                    int64_t n4, float alpha, KTrace tr, KTrace tg) {
+  ktrace_begin(tr);
+  ktrace_begin(tg);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kApplyUnroll - 1) * stride < n4; i += kApplyUnroll * stride) {
@@ -136,6 +138,11 @@ __global__ void ps_apply_vec_kernel(const float4* __restrict__ g, float4* __rest
     wv.z = fmaf(alpha, gv.z, wv.z);
     wv.w = fmaf(alpha, gv.w, wv.w);
     W[i] = wv;
+  }
+  if (tr.rec || tg.rec) {
+    __syncthreads();
+    ktrace_end(tr);
+    ktrace_end(tg);
   }
 }
 
@@ -226,15 +233,22 @@ cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s) {
+int ps_apply_grid(int64_t count) {
+  const int64_t n4 = count / 4;
+  return n4 > 0 ? grid_for((n4 + kApplyUnroll - 1) / kApplyUnroll, 256) : 0;
+}
+
+cudaError_t launch_ps_apply(const float* g, float* W, int64_t count, float alpha, cudaStream_t s,
+                            KTrace tr, KTrace tg) {
   clear_stale_launch_error();
   const int threads = 256;
   if (aligned16(g) && aligned16(W)) {
     const int64_t n4 = count / 4;
+    const int grid = ps_apply_grid(count);
+    if (tr.rec && tr.expected == 0) tr.expected = (unsigned)grid;
     if (n4 > 0)
-      ps_apply_vec_kernel<<<grid_for((n4 + kApplyUnroll - 1) / kApplyUnroll, threads), threads, 0,
-                            s>>>(reinterpret_cast<const float4*>(g), reinterpret_cast<float4*>(W),
-                                 n4, alpha);
+      ps_apply_vec_kernel<<<grid, threads, 0, s>>>(reinterpret_cast<const float4*>(g),
+                                                   reinterpret_cast<float4*>(W), n4, alpha, tr, tg);
     const int64_t rem = count - n4 * 4;
     if (rem > 0)
       ps_apply_scalar_kernel<<<1, 32, 0, s>>>(g + n4 * 4, W + n4 * 4, rem, alpha);
@@ -252,6 +266,23 @@ cudaError_t launch_sim_ps_reduce_apply(const float* const* grads, int P, float* 
   const int threads = 256;
   sim_ps_reduce_apply_kernel<<<grid_for(n, threads), threads, 0, s>>>(gp, P, W, n, alpha);
   return cudaGetLastError();
+}
+
+__global__ void ktrace_init_kernel(unsigned long long* rec) {
+  if (threadIdx.x < kTraceWords) rec[threadIdx.x] = threadIdx.x == 0 ? ~0ull : 0ull;
+}
+
+cudaError_t ktrace_alloc(unsigned long long** rec) {
+  cudaError_t e = cudaMalloc(rec, kTraceWords * sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  return ktrace_reset(*rec);
+}
+
+cudaError_t ktrace_reset(unsigned long long* rec) {
+  clear_stale_launch_error();
+  ktrace_init_kernel<<<1, 32>>>(rec);
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? e : cudaDeviceSynchronize();
 }
 
 }  // namespace pos

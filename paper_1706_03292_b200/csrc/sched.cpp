@@ -60,6 +60,8 @@ struct Unit {
   bool has_plan = false;
   int plan_ctas = -1;
   unsigned int* tile_counter = nullptr;   // dynamic tile scheduler state of this unit's launches
+  unsigned long long* trace = nullptr;    // POS_SCHED_TRACE: device-side record of the apply kernel
+  int trace_grid = 0;                     // CTAs of one traced launch (0 = nothing traced)
   std::vector<int> members;    // layer indices (forward order)
   int pending = 0;             // members not yet triggered in this iteration
   const void* u = nullptr;     // FC factors of this iteration
@@ -103,6 +105,10 @@ struct pos_sched {
   int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1: one, in order)
   int n_sfb = 0;              // SFB units registered
   bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
+  // POS_SCHED_TRACE: one group record per scheme (all of a step's PS / SFB apply kernels)
+  unsigned long long* group[2] = {nullptr, nullptr};
+  unsigned group_expected[2] = {0, 0};
+  int traced_ctas = -2;       // max_ctas the traced grids were computed for
 };
 
 using namespace pos;
@@ -110,6 +116,68 @@ using namespace pos;
 namespace {
 
 bool timing_full(const pos_sched* s) { return (s->flags & POS_SCHED_TIMING) != 0; }
+bool tracing(const pos_sched* s) { return (s->flags & POS_SCHED_TRACE) != 0; }
+
+// (re)build the cached tensor-core launch plan of an SFB unit for the context's current CTA cap
+int ensure_plan(pos_sched* s, Unit& un) {
+  pos_ctx* c = s->ctx;
+  if (un.scheme != POS_SCHEME_SFB || un.plan_ctas == c->max_ctas) return POS_OK;
+  un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * c->world, un.dtype, un.gbuf, un.W,
+                                 un.N, c->max_ctas, un.b, un.flag_mode ? un.gbuf2 : nullptr);
+  un.plan.counter = (s->flags & POS_SCHED_STATIC_TILES) ? nullptr : un.tile_counter;
+  un.plan.gsel = un.flag_mode ? un.gstate : nullptr;
+  if (un.flag_mode && !un.has_plan) POS_FAIL(POS_ESTATE, "flag-mode gather without a tensor-core plan");
+  un.plan_ctas = c->max_ctas;
+  return POS_OK;
+}
+
+// Device-side tracing: every unit's apply kernel stamps its own record; the apply kernels of one
+// step also stamp the group record of their scheme, whose interval is the sum of their grids.
+int prepare_tracing(pos_sched* s) {
+  pos_ctx* c = s->ctx;
+  if (s->traced_ctas == c->max_ctas) return POS_OK;
+  unsigned exp[2] = {0, 0};
+  bool complete[2] = {true, true};
+  for (auto& un : s->units) {
+    int rc = ensure_plan(s, un);
+    if (rc) return rc;
+    if (!un.trace) POS_CUDA_TRY(ktrace_alloc(&un.trace));
+    const int sc = un.scheme == POS_SCHEME_SFB ? 1 : 0;
+    if (un.scheme == POS_SCHEME_SFB)
+      un.trace_grid = un.has_plan ? un.plan.grid : 0;        // the SIMT path is not traced
+    else
+      un.trace_grid = ps_stage_grid(c, un.n, un.grad, un.W);
+    if (un.trace_grid > 0) exp[sc] += (unsigned)un.trace_grid;
+    else if (un.scheme == POS_SCHEME_SFB) complete[sc] = false;
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (!s->group[k]) POS_CUDA_TRY(ktrace_alloc(&s->group[k]));
+    POS_CUDA_TRY(ktrace_reset(s->group[k]));
+    s->group_expected[k] = complete[k] ? exp[k] : 0;
+  }
+  for (auto& un : s->units) POS_CUDA_TRY(ktrace_reset(un.trace));
+  s->traced_ctas = c->max_ctas;
+  return POS_OK;
+}
+
+KTrace unit_trace(const pos_sched* s, const Unit& un) {
+  KTrace t;
+  if (tracing(s) && un.trace && un.trace_grid > 0) {
+    t.rec = un.trace;
+    t.expected = (unsigned)un.trace_grid;
+  }
+  return t;
+}
+
+KTrace group_trace(const pos_sched* s, int scheme) {
+  KTrace t;
+  const int k = scheme == POS_SCHEME_SFB ? 1 : 0;
+  if (tracing(s) && s->group[k] && s->group_expected[k] > 0) {
+    t.rec = s->group[k];
+    t.expected = s->group_expected[k];
+  }
+  return t;
+}
 bool timing_any(const pos_sched* s) {
   return (s->flags & (POS_SCHED_TIMING | POS_SCHED_TIMING_APPLY)) != 0;
 }
@@ -244,17 +312,12 @@ int issue_unit(pos_sched* s, int ui) {
     if (un.kind == POS_KIND_FC && ev_wfree != l0.ev_in)
       POS_CUDA_TRY(cudaStreamWaitEvent(as, ev_wfree, 0));
     if (ts && (rc = trec(ts->a0, as))) return rc;
-    if (un.plan_ctas != c->max_ctas) {   // (re)build the cached launch plan
-      un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * P, un.dtype, un.gbuf, un.W,
-                                     un.N, c->max_ctas, un.b, un.flag_mode ? un.gbuf2 : nullptr);
-      un.plan.counter = (s->flags & POS_SCHED_STATIC_TILES) ? nullptr : un.tile_counter;
-      un.plan.gsel = un.flag_mode ? un.gstate : nullptr;
-      if (un.flag_mode && !un.has_plan)
-        POS_FAIL(POS_ESTATE, "flag-mode gather without a tensor-core plan");
-      un.plan_ctas = c->max_ctas;
-    }
+    if ((rc = ensure_plan(s, un))) return rc;
     if (un.has_plan) {
-      cudaError_t e2 = sfb_tc_launch(un.plan, s->alpha, 1, as);   // bias fused
+      SfbTcPlan pl = un.plan;
+      pl.trace = unit_trace(s, un);
+      pl.group = group_trace(s, POS_SCHEME_SFB);
+      cudaError_t e2 = sfb_tc_launch(pl, s->alpha, 1, as);   // bias fused
       if (e2 != cudaSuccess) return ctx_cuda_fail(c, e2, "reconstruct launch");
     } else {
       rc = reconstruct_apply(un.M, un.N, un.K * P, un.dtype, un.gbuf, 1, un.W, un.N, un.b,
@@ -274,7 +337,8 @@ int issue_unit(pos_sched* s, int ui) {
     }
     if (ts && (rc = trec(ts->packed, cs))) return rc;
     rc = stage_ps_dense(c, un.n, un.grad, un.W, s->alpha, cs, ts ? ts->a0 : nullptr,
-                        ts ? ts->a1 : nullptr, /*zero_tail=*/false);
+                        ts ? ts->a1 : nullptr, /*zero_tail=*/false, unit_trace(s, un),
+                        group_trace(s, POS_SCHEME_PS));
     if (rc != POS_OK) return rc;
     if (ts && (rc = trec(ts->done, cs))) return rc;
     POS_CUDA_TRY(cudaEventRecord(un.ev_done, cs));
@@ -346,7 +410,7 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   POS_CHECK_ARG(n_layers >= 1, "n_layers must be >= 1");
   POS_CHECK_ARG((flags & ~(POS_SCHED_TIMING | POS_SCHED_SEQUENTIAL | POS_SCHED_TIMING_APPLY |
                             POS_SCHED_NO_SYMM | POS_SCHED_PS_AFTER_SFB |
-                            POS_SCHED_STATIC_TILES)) == 0,
+                            POS_SCHED_STATIC_TILES | POS_SCHED_TRACE)) == 0,
                 "unknown flags");
   POS_CHECK_ARG(!c->local || c->world == 1, "the scheduler needs a real (or 1-worker) context");
   pos_sched* s = new pos_sched();
@@ -489,6 +553,7 @@ int pos_sched_begin(pos_sched* s, float alpha) {
     if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d was never added", l);
   int rc = ctx_check(s->ctx);
   if (rc) return rc;
+  if (tracing(s) && (rc = prepare_tracing(s))) return rc;
   for (auto& ly : s->layers) ly.triggered = false;   // C := 0
   for (auto& un : s->units) un.pending = (int)un.members.size();
   s->order.clear();
@@ -655,6 +720,82 @@ int pos_sched_timing_span(pos_sched* s, int32_t scheme, float* span_ms) {
   return n;
 }
 
+int pos_sched_timeline(pos_sched* s, float* out, int32_t max_units) {
+  clear_error();
+  POS_CHECK_ARG(s && out && max_units >= 0, "bad arguments");
+  if (!timing_full(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TIMING");
+  const int nu = (int)s->units.size();
+  // the most recent iteration slot that every unit has recorded
+  int slot = -1;
+  for (int k = 0; k < kTRing && slot < 0; ++k) {
+    const int t = (int)(((s->iter - 1 - k) % kTRing + kTRing) % kTRing);
+    bool all = true;
+    for (auto& un : s->units) all = all && un.ring[t].used;
+    if (all) slot = t;
+  }
+  if (slot < 0) POS_FAIL(POS_ESTATE, "no iteration with live timing events");
+  const cudaEvent_t ref = s->units[s->order.empty() ? 0 : s->order[0]].ring[slot].start;
+  POS_CUDA_TRY(cudaEventSynchronize(ref));
+  for (int u = 0; u < nu && u < max_units; ++u) {
+    const TSlot& t = s->units[u].ring[slot];
+    const cudaEvent_t ev[6] = {t.start, t.packed, t.gathered, t.a0, t.a1, t.done};
+    for (int k = 0; k < 6; ++k) {
+      float ms = -1.0f;
+      if (ev[k] && !(k == 2 && s->units[u].scheme != POS_SCHEME_SFB)) {
+        POS_CUDA_TRY(cudaEventSynchronize(ev[k]));
+        POS_CUDA_TRY(cudaEventElapsedTime(&ms, ref, ev[k]));
+      }
+      out[6 * u + k] = ms;
+    }
+  }
+  return nu;
+}
+
+static int read_trace(const unsigned long long* rec, double* avg_us, double* last_us,
+                      int64_t* n) {
+  unsigned long long h[kTraceWords];
+  POS_CUDA_TRY(cudaMemcpy(h, rec, sizeof(h), cudaMemcpyDeviceToHost));
+  if (n) *n = (int64_t)h[3];
+  if (avg_us) *avg_us = h[3] ? (double)h[4] / (double)h[3] * 1e-3 : 0.0;
+  if (last_us) *last_us = h[3] ? (double)(h[6] - h[5]) * 1e-3 : 0.0;
+  return POS_OK;
+}
+
+int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, int64_t* launches) {
+  clear_error();
+  int rc = check_layer(s, l);
+  if (rc) return rc;
+  if (!tracing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TRACE");
+  if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
+  const Unit& un = s->units[s->layers[l].unit];
+  if (!un.trace) POS_FAIL(POS_ESTATE, "no traced iteration yet");
+  POS_CUDA_TRY(cudaDeviceSynchronize());
+  return read_trace(un.trace, avg_us, last_us, launches);
+}
+
+int pos_sched_trace_span(pos_sched* s, int32_t scheme, double* avg_us, int64_t* steps) {
+  clear_error();
+  POS_CHECK_ARG(s && (scheme == POS_SCHEME_SFB || scheme == POS_SCHEME_PS), "bad arguments");
+  if (!tracing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TRACE");
+  const int k = scheme == POS_SCHEME_SFB ? 1 : 0;
+  if (!s->group[k] || s->group_expected[k] == 0)
+    POS_FAIL(POS_ESTATE, "no traced group for scheme %d (no units, or an untraced SIMT path)", scheme);
+  POS_CUDA_TRY(cudaDeviceSynchronize());
+  return read_trace(s->group[k], avg_us, nullptr, steps);
+}
+
+int pos_sched_trace_reset(pos_sched* s) {
+  clear_error();
+  POS_CHECK_ARG(s, "bad arguments");
+  if (!tracing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TRACE");
+  POS_CUDA_TRY(cudaDeviceSynchronize());
+  for (auto& un : s->units)
+    if (un.trace) POS_CUDA_TRY(ktrace_reset(un.trace));
+  for (auto* g : s->group)
+    if (g) POS_CUDA_TRY(ktrace_reset(g));
+  return POS_OK;
+}
+
 int pos_sched_timing_reset(pos_sched* s) {
   clear_error();
   POS_CHECK_ARG(s, "NULL scheduler");
@@ -697,11 +838,14 @@ int pos_sched_destroy(pos_sched* s) {
       else cudaFree(un.gbuf);
     }
     if (un.tile_counter) cudaFree(un.tile_counter);
+    if (un.trace) cudaFree(un.trace);
     if (un.gstate) cudaFree(un.gstate);
   }
   for (auto st : s->pool)
     if (st) cudaStreamDestroy(st);
   if (s->ev_end) cudaEventDestroy(s->ev_end);
+  for (auto* g : s->group)
+    if (g) cudaFree(g);
   delete s;
   return POS_OK;
 }

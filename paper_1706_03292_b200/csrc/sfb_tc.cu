@@ -335,6 +335,7 @@ struct TileInfo {
   unsigned int* counter;
   float* bias;     // fused A4b: b (+)= alpha * accumulator column N; nullptr = no bias
   const unsigned* gsel;   // double-buffered gather: buffer (*gsel - 1) & 1; nullptr = buffer 0
+  KTrace trace, group;    // device-side launch trace (off when rec == nullptr)
 };
 
 template <bool kTF32, bool kPair>
@@ -394,6 +395,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ktrace_begin(ti.trace);
+  ktrace_begin(ti.group);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < ST; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, 1); }
@@ -662,6 +665,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all(); else __syncthreads();
+  ktrace_end(ti.trace);                       // thread 0: every role of this CTA is done
+  ktrace_end(ti.group);
   if (warp == 1) {
     tc_fence_after();
     if constexpr (kPair)
@@ -821,6 +826,9 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   ti.counter = pl.counter;
   ti.bias = pl.bias;
   ti.gsel = pl.gsel;
+  ti.trace = pl.trace;
+  if (ti.trace.rec && ti.trace.expected == 0) ti.trace.expected = (unsigned)pl.grid;
+  ti.group = pl.group;
   if constexpr (kPair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.grid);

@@ -184,6 +184,7 @@ struct PsArgs {
   int P;
   int64_t lo, hi;               // this rank's shard
   float alpha;
+  KTrace trace, group;          // device-side launch trace (tracing scheduler)
 };
 
 template <bool kRedMc>
@@ -228,8 +229,12 @@ __device__ __forceinline__ void ps_st1(const PsArgs& a, int64_t j, float v) {
 
 template <bool kRedMc, bool kStMc>
 __global__ void __launch_bounds__(kPsThreads) ps_sync_kernel(PsArgs a, Xg x) {
+  ktrace_begin(a.trace);
+  ktrace_begin(a.group);
   if (!xg_enter(x)) return;
-  const int64_t v0 = a.lo / 4, v1 = a.hi / 4;   // lo is a multiple of 64
+  // lo is a multiple of 64 for a non-empty shard; an empty shard (lo == hi == n, a trailing rank of
+  // a small unit) does no work but still takes part in the barriers
+  const int64_t v0 = a.lo / 4, v1 = a.lo < a.hi ? a.hi / 4 : v0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kPsUnroll - 1) * stride < v1; i += kPsUnroll * stride) {
@@ -258,9 +263,14 @@ __global__ void __launch_bounds__(kPsThreads) ps_sync_kernel(PsArgs a, Xg x) {
     ps_st4<kStMc>(a, i, w);
   }
   if (blockIdx.x == 0)   // scalar tail of the shard
-    for (int64_t j = v1 * 4 + threadIdx.x; j < a.hi; j += blockDim.x)
+    for (int64_t j = std::max(v1 * 4, a.lo) + threadIdx.x; j < a.hi; j += blockDim.x)
       ps_st1<kStMc>(a, j, fmaf(a.alpha, ps_red1<kRedMc>(a, j), a.wl[j]));
   xg_exit(x);
+  if (a.trace.rec || a.group.rec) {
+    __syncthreads();
+    ktrace_end(a.trace);
+    ktrace_end(a.group);
+  }
 }
 
 __device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
@@ -419,8 +429,9 @@ Xg no_xg(pos_ctx* c) {
 }
 
 template <bool kRedMc, bool kStMc>
-cudaError_t launch_ps(int grid, cudaStream_t s, const PsArgs& a, const Xg& x) {
+cudaError_t launch_ps(int grid, cudaStream_t s, PsArgs a, const Xg& x) {
   clear_stale_launch_error();
+  if (a.trace.rec && a.trace.expected == 0) a.trace.expected = (unsigned)grid;
   ps_sync_kernel<kRedMc, kStMc><<<grid, kPsThreads, 0, s>>>(a, x);
   return cudaGetLastError();
 }
@@ -485,11 +496,13 @@ static int register_window(pos_ctx* c, SymmState* st, void* p, size_t bytes, Sym
   out->base = static_cast<char*>(p);
   out->bytes = bytes;
   out->win = win;
-  for (int q = 0; q < c->world; ++q) out->peer[q] = htab[q];
+  // peers through NCCL's flat LSA mapping; this rank through the allocation's own address (the
+  // same physical memory — keeps local accesses on the regular mapping)
+  for (int q = 0; q < c->world; ++q) out->peer[q] = q == c->rank ? out->base : htab[q];
   out->mc = htab[c->world];
-  if (!out->mc || out->peer[c->rank] != out->base) {
+  if (!out->mc || !htab[c->rank]) {
     ncclCommWindowDeregister(c->comm, win);
-    POS_FAIL(POS_EUNSUPPORTED, "symmetric window without multicast / consistent local address");
+    POS_FAIL(POS_EUNSUPPORTED, "symmetric window without a multicast / peer mapping");
   }
   return POS_OK;
 }
@@ -575,8 +588,10 @@ bool symm_lookup(pos_ctx* c, const void* p, size_t bytes) {
   return symm_find(c, p, bytes, &off) != nullptr;
 }
 
+int symm_ps_grid(pos_ctx* c, int64_t n) { return ps_grid(c, n, c->world); }
+
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done) {
+                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr, KTrace tg) {
   *done = false;
   const int P = c->world;
   if (P < 2 || c->local) return POS_OK;
@@ -595,6 +610,8 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   a.wl = W;
   a.P = P;
   a.alpha = alpha;
+  a.trace = tr;
+  a.group = tg;
   pos_shard_range(n, P, c->rank, &a.lo, &a.hi);
   const Xg x = make_xg(c, kSitePsEntry);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));

@@ -458,3 +458,71 @@ def test_sched_wait_host_timeout():
     assert float(W[0]) == 1.0
     sch.close()
     ctx.close()
+
+
+def test_sched_device_trace():
+    """POS_SCHED_TRACE: the apply kernels stamp %globaltimer into device records (no events in the
+    streams): every unit reports one launch per iteration with a positive duration, the SFB span of
+    a step covers its longest reconstruction, and the results are unchanged (oracle, bitwise) —
+    also under CUDA-graph replay."""
+    model = make_model(6)
+    a = si.EXACT_ALPHA
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, len(model), trace=True)
+    dev = []
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            n = d["n"]
+            W = torch.zeros(pos.pos_padded_size(n, 1), device="cuda"); W[:n] = to_dev(d["W"])
+            G = torch.zeros_like(W); G[:n] = to_dev(d["g"])
+            sch.add_dense(l, n, W, G)
+            dev.append({"W": W, "G": G})
+        else:
+            W, b = to_dev(d["W"]), to_dev(d["b"])
+            sch.add_fc(l, d["M"], d["N"], d["K"], W, b, None, "bf16", pos.POS_IN_BF16)
+            dev.append({"W": W, "b": b, "u": to_dev(d["u"], "bf16"), "v": to_dev(d["v"], "bf16")})
+
+    def step(stream):
+        sch.begin(a)
+        for l in reversed(range(len(model))):
+            if model[l]["kind"] == "dense":
+                sch.grad_ready(l, stream)
+            else:
+                sch.factors_ready(l, dev[l]["u"], dev[l]["v"], stream)
+        sch.end(stream)
+
+    step(torch.cuda.current_stream())              # first iteration eager (allocates records)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+        step(torch.cuda.current_stream())
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    durs = []
+    for l in range(len(model)):
+        avg, last, n = sch.trace(l)
+        assert n == 3 and avg > 0 and last > 0, (l, avg, last, n)
+        durs.append(avg)
+    span, steps = sch.trace_span(pos.POS_SCHEME_SFB)
+    assert steps == 3
+    sfb = [t for t, d in zip(durs, model) if d["kind"] != "dense"]
+    assert span >= 0.99 * max(sfb)
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            r = d["W"]
+            for _ in range(3):
+                r = sync.ps_update(r, [d["g"]], a)
+            assert np.array_equal(to_host(dev[l]["W"][:d["n"]]), r)
+        else:
+            Wr, br = d["W"], d["b"]
+            for _ in range(3):
+                Wr, br = sync.sfb_update(Wr, br, [d["u"]], [d["v"]], a)
+            assert np.array_equal(to_host(dev[l]["W"]), Wr) and np.array_equal(to_host(dev[l]["b"]), br)
+    sch.trace_reset()
+    assert sch.trace(0)[2] == 0
+    g = None
+    sch.close()
+    ctx.close()

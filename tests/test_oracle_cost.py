@@ -215,3 +215,28 @@ def test_b200_model_limits_and_monotonicity():
             assert not (seen_ps and s == cost.SFB), (M, N, P, K)
     # the symmetric formula (reading S7)
     assert cost.b200_times(300, 7000, 64, 8) == cost.b200_times(7000, 300, 64, 8)
+
+
+def test_b200_model_tensor_term_pinned_to_an_independent_flop_count():
+    """The tensor-core term of b200_times (2 M N K P / F_tc) pinned to torch's own flop counter on
+    the contraction the method performs: the P workers' K factor rows stacked (Eq. 2) and
+    contracted as U^T V. Checked where the term dominates (K P = 2048 > 4 F_tc / B_hbm ~ 1004) and
+    where the HBM term does (K P = 64), so a K-vs-K*P slip or a dropped factor 2 fails."""
+    import torch
+    from torch.utils.flop_counter import FlopCounterMode
+    from fractions import Fraction
+    hbm, tc = 6551e9, 1644e12
+    for (M, N, K, P) in [(96, 160, 256, 8), (4096, 4096, 256, 8), (64, 48, 8, 8)]:
+        U = torch.empty(K * P, M, device="meta")
+        V = torch.empty(K * P, N, device="meta")
+        with FlopCounterMode(display=False) as fc:
+            U.t() @ V
+        flops = fc.get_total_flops()
+        t_sfb, _ = cost.b200_times(M, N, K, P, hbm=hbm, nvl=None, tc=tc)
+        t_tc = Fraction(flops) / Fraction(tc)
+        t_hbm = Fraction(8 * M * N) / Fraction(hbm)
+        assert t_sfb == max(t_tc, t_hbm), (M, N, K, P)
+        if K * P > 1004:
+            assert t_sfb == t_tc            # tensor-bound regime
+        else:
+            assert t_sfb == t_hbm
