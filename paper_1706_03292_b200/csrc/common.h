@@ -14,6 +14,10 @@
 
 #include "poseidon.h"
 
+#ifdef __CUDACC__
+#include <cuda_bf16.h>
+#endif
+
 namespace pos {
 
 // thread-local last-error message (pos_last_error)
@@ -115,6 +119,65 @@ __device__ __forceinline__ void ktrace_end(const KTrace& t) {
     atomicExch(t.rec + 2, 0ull);
     __threadfence();
   }
+}
+
+// ---- A2 factor pack: one 16-byte output vector of a gathered row ----
+// Output elements idx .. idx+VEC-1 of the u or v part (VEC = 8 bf16 / 4 fp32); src = the input row
+// (u_k or v_k), lim = its length (M or N), onec = the ones column (N for the v part, -1 for u).
+// Chunks entirely inside the row whose source is suitably aligned take vector loads (16 B for
+// 8 bf16 / 4 fp32 inputs, 2 x 16 B for 8 fp32 inputs, 8 B for 4 bf16 inputs); the row tail, the
+// pad and unaligned rows (M or N not a multiple of the vector) take element loads.
+__device__ __forceinline__ float pack_ld1(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float pack_ld1(const float* p) { return *p; }
+template <typename Tin, bool kBF16>
+__device__ __forceinline__ uint4 pack_chunk(const Tin* __restrict__ src, int64_t idx, int64_t lim,
+                                            int64_t onec) {
+  constexpr int VEC = kBF16 ? 8 : 4;
+  const Tin* p = src + idx;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if (idx + VEC <= lim) {
+    if constexpr (kBF16 && sizeof(Tin) == 2) {          // bf16 -> bf16: a straight copy
+      if ((a & 15u) == 0) return __ldg(reinterpret_cast<const uint4*>(p));
+    } else if constexpr (kBF16) {                        // fp32 -> bf16
+      if ((a & 15u) == 0) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(p));
+        const float4 y = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        uint4 o;
+        __nv_bfloat162 h;
+        h = __floats2bfloat162_rn(x.x, x.y); o.x = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(x.z, x.w); o.y = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(y.x, y.y); o.z = *reinterpret_cast<uint32_t*>(&h);
+        h = __floats2bfloat162_rn(y.z, y.w); o.w = *reinterpret_cast<uint32_t*>(&h);
+        return o;
+      }
+    } else if constexpr (sizeof(Tin) == 4) {             // fp32 -> fp32
+      if ((a & 15u) == 0) return __ldg(reinterpret_cast<const uint4*>(p));
+    } else {                                             // bf16 -> fp32
+      if ((a & 7u) == 0) {
+        const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+        uint4 o;
+        o.x = x.x << 16; o.y = x.x & 0xFFFF0000u;
+        o.z = x.y << 16; o.w = x.y & 0xFFFF0000u;
+        return o;
+      }
+    }
+  }
+  uint4 o;
+  if constexpr (kBF16) {
+    __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      h[i] = __float2bfloat16_rn(idx + i < lim ? pack_ld1(p + i) : (idx + i == onec ? 1.f : 0.f));
+    o = *reinterpret_cast<const uint4*>(h);
+  } else {
+    float f[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      f[i] = idx + i < lim ? pack_ld1(p + i) : (idx + i == onec ? 1.f : 0.f);
+    o = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                   __float_as_uint(f[3]));
+  }
+  return o;
 }
 #endif
 

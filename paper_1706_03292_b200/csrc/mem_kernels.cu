@@ -1,5 +1,5 @@
 // HBM-bound kernels of the hot path:
-//   A2  factor pack      u, v (autograd layout) -> gathered row [u | 0 pad | v | 0 pad] in dtype
+//   A2  factor pack      u, v (autograd layout) -> gathered row [u | 0 pad | v | 1, 0 pad] in dtype
 //   A4b bias column sum  b (+)= alpha * sum_j U[j][m], fixed order (deterministic)
 //   A7  PS shard apply   W += alpha * g, 16-byte vectors, grid-stride
 //   sim PS reduce-apply  W += alpha * sum_p g_p (the simulated-P stand-in for RS + A7 + AG)
@@ -16,19 +16,19 @@ namespace {
 
 __device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ float ld_in(const float* p) { return *p; }
-
 // ---------------------------------------------------------------------------------------------
 // A2: one thread writes one 16-byte output vector. grid.y = sample row k (K <= 65535 per launch
 // chunk). The input rows are read with plain (unaligned-safe) loads; consecutive threads read
 // consecutive elements, so the reads coalesce.
 // ---------------------------------------------------------------------------------------------
-template <typename Tin>
-__global__ void pack_bf16_kernel(const Tin* __restrict__ u, const Tin* __restrict__ v,
-                                 __nv_bfloat16* __restrict__ out, int64_t M, int64_t N,
-                                 int64_t Mp, int64_t R, int64_t k0) {
+template <typename Tin, bool kBF16>
+__global__ void pack_kernel(const Tin* __restrict__ u, const Tin* __restrict__ v,
+                            void* __restrict__ out, int64_t M, int64_t N, int64_t Mp, int64_t R,
+                            int64_t k0) {
+  constexpr int VEC = kBF16 ? 8 : 4;
   const int64_t k = k0 + blockIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 8-element chunk in row
-  const int64_t col = c * 8;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // VEC-element chunk in row
+  const int64_t col = c * VEC;
   if (col >= R) return;
   const Tin* src;
   int64_t idx, lim;
@@ -37,36 +37,9 @@ __global__ void pack_bf16_kernel(const Tin* __restrict__ u, const Tin* __restric
   // v's first pad column (index N) holds 1.0: the reconstruction's extra output column is then
   // sum_j u_j, the bias gradient (A4b fused into A4); every other pad element is 0
   const int64_t onec = col < Mp ? -1 : N;
-  __align__(16) __nv_bfloat16 o[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t j = idx + i;
-    o[i] = __float2bfloat16_rn(j < lim ? ld_in(src + j) : (j == onec ? 1.0f : 0.0f));
-  }
-  *reinterpret_cast<uint4*>(out + k * R + col) = *reinterpret_cast<const uint4*>(o);
-}
-
-template <typename Tin>
-__global__ void pack_f32_kernel(const Tin* __restrict__ u, const Tin* __restrict__ v,
-                                float* __restrict__ out, int64_t M, int64_t N, int64_t Mp,
-                                int64_t R, int64_t k0) {
-  const int64_t k = k0 + blockIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 4-element chunk
-  const int64_t col = c * 4;
-  if (col >= R) return;
-  const Tin* src;
-  int64_t idx, lim;
-  if (col < Mp) { src = u + k * M; idx = col; lim = M; }
-  else          { src = v + k * N; idx = col - Mp; lim = N; }
-  // v's first pad column (index N) holds 1.0: the reconstruction's extra output column is then
-  // sum_j u_j, the bias gradient (A4b fused into A4); every other pad element is 0
-  const int64_t onec = col < Mp ? -1 : N;
-  float4 o;
-  o.x = idx + 0 < lim ? ld_in(src + idx + 0) : (idx + 0 == onec ? 1.0f : 0.0f);
-  o.y = idx + 1 < lim ? ld_in(src + idx + 1) : (idx + 1 == onec ? 1.0f : 0.0f);
-  o.z = idx + 2 < lim ? ld_in(src + idx + 2) : (idx + 2 == onec ? 1.0f : 0.0f);
-  o.w = idx + 3 < lim ? ld_in(src + idx + 3) : (idx + 3 == onec ? 1.0f : 0.0f);
-  *reinterpret_cast<float4*>(out + k * R + col) = o;
+  const int64_t eb = kBF16 ? 2 : 4;
+  *reinterpret_cast<uint4*>(static_cast<char*>(out) + (k * R + col) * eb) =
+      pack_chunk<Tin, kBF16>(src, idx, lim, onec);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -194,26 +167,14 @@ cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtyp
   for (int64_t k0 = 0; k0 < K; k0 += 65535) {
     const unsigned rows = (unsigned)std::min<int64_t>(65535, K - k0);
     dim3 grid((unsigned)((chunks + threads - 1) / threads), rows);
+    using bf = __nv_bfloat16;
+    const bool in_bf = in_dtype == POS_IN_BF16;
     if (dtype == POS_DT_BF16) {
-      auto* out = static_cast<__nv_bfloat16*>(slot);
-      if (in_dtype == POS_IN_BF16)
-        pack_bf16_kernel<<<grid, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(u),
-                                                  static_cast<const __nv_bfloat16*>(v), out, M, N,
-                                                  Mp, R, k0);
-      else
-        pack_bf16_kernel<<<grid, threads, 0, s>>>(static_cast<const float*>(u),
-                                                  static_cast<const float*>(v), out, M, N, Mp, R,
-                                                  k0);
+      if (in_bf) pack_kernel<bf, true><<<grid, threads, 0, s>>>(static_cast<const bf*>(u), static_cast<const bf*>(v), slot, M, N, Mp, R, k0);
+      else       pack_kernel<float, true><<<grid, threads, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(v), slot, M, N, Mp, R, k0);
     } else {
-      auto* out = static_cast<float*>(slot);
-      if (in_dtype == POS_IN_BF16)
-        pack_f32_kernel<<<grid, threads, 0, s>>>(static_cast<const __nv_bfloat16*>(u),
-                                                 static_cast<const __nv_bfloat16*>(v), out, M, N,
-                                                 Mp, R, k0);
-      else
-        pack_f32_kernel<<<grid, threads, 0, s>>>(static_cast<const float*>(u),
-                                                 static_cast<const float*>(v), out, M, N, Mp, R,
-                                                 k0);
+      if (in_bf) pack_kernel<bf, false><<<grid, threads, 0, s>>>(static_cast<const bf*>(u), static_cast<const bf*>(v), slot, M, N, Mp, R, k0);
+      else       pack_kernel<float, false><<<grid, threads, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(v), slot, M, N, Mp, R, k0);
     }
   }
   return cudaGetLastError();

@@ -273,9 +273,6 @@ __global__ void __launch_bounds__(kPsThreads) ps_sync_kernel(PsArgs a, Xg x) {
   }
 }
 
-__device__ __forceinline__ float ld_in(const __nv_bfloat16* p) { return __bfloat162float(*p); }
-__device__ __forceinline__ float ld_in(const float* p) { return *p; }
-
 // One rank's factor pack + gather. Byte addresses of THIS rank's slot in buffer 0 / 1.
 struct PackArgs {
   const void* u;
@@ -319,20 +316,10 @@ __global__ void __launch_bounds__(256) pack_x_kernel(PackArgs a, Xg x) {
     int64_t idx, lim;
     if (col < a.Mp) { src = u + k * a.M; idx = col; lim = a.M; }
     else            { src = v + k * a.N; idx = col - a.Mp; lim = a.N; }
-    const int64_t onec = col < a.Mp ? -1 : a.N;   // ones column (fused bias), as in pack_*_kernel
-    float4 o;
-    if constexpr (kBF16) {
-      __align__(16) __nv_bfloat16 h[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        h[i] = __float2bfloat16_rn(idx + i < lim ? ld_in(src + idx + i) : (idx + i == onec ? 1.f : 0.f));
-      o = *reinterpret_cast<const float4*>(h);   // bit pattern only; a store does not convert
-    } else {
-      o.x = idx + 0 < lim ? ld_in(src + idx + 0) : (idx + 0 == onec ? 1.f : 0.f);
-      o.y = idx + 1 < lim ? ld_in(src + idx + 1) : (idx + 1 == onec ? 1.f : 0.f);
-      o.z = idx + 2 < lim ? ld_in(src + idx + 2) : (idx + 2 == onec ? 1.f : 0.f);
-      o.w = idx + 3 < lim ? ld_in(src + idx + 3) : (idx + 3 == onec ? 1.f : 0.f);
-    }
+    const int64_t onec = col < a.Mp ? -1 : a.N;   // ones column (fused bias), as in pack_kernel
+    const uint4 q = pack_chunk<Tin, kBF16>(src, idx, lim, onec);
+    const float4 o = make_float4(__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
+                                 __uint_as_float(q.w));   // bit pattern only; stores do not convert
     const int64_t boff = (k * a.R + col) * EB;   // byte offset of this vector in the slot
     if constexpr (kMc) {
       mm_st_v4(reinterpret_cast<float*>(a.mc[b] + boff), o);
