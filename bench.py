@@ -442,10 +442,12 @@ def run_ours(a):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * 1 + rank)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
-    # in-step kernel times come from device-side tracing (the kernels stamp %globaltimer): no
-    # timing events in the captured step; --layers adds per-stage events and a timeline
+    # The timed region replays UNTRACED step graphs. In-step kernel times come from a second ring
+    # of the same step captured with device-side tracing (the kernels stamp %globaltimer; no timing
+    # events in the captured step), replayed after the timed region; --layers adds per-stage events
+    # and a timeline; --no-trace times the apply stages with CUDA events instead
     sch = pos.Scheduler(ctx, L, timing=(True if a.layers else ("apply" if a.no_trace else False)),
-                        trace=not a.no_trace, sequential=a.sequential,
+                        trace=False, sequential=a.sequential,
                         symm=not a.no_symm, ps_after_sfb=a.ps_after_sfb, static_tiles=a.static_tiles)
     bufs = register_units(pos, ctx, sch, model, units, K, a.dtype, device_fill(gen, a.dtype),
                           symm=not a.no_symm)
@@ -482,8 +484,6 @@ def run_ours(a):
     torch.cuda.synchronize()
     if a.layers or a.no_trace:
         sch.timing_reset()
-    if not a.no_trace:
-        sch.trace_reset()
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -516,16 +516,46 @@ def run_ours(a):
     # span of the reconstructions within the step (they overlap: two streams) — before timing(),
     # which retires the events in eager mode
     has_fc, has_dense = any(u["kind"] == "fc" for u in units), any(u["kind"] == "dense" for u in units)
+    traced_ms = None
     if a.no_trace:    # CUDA-event timing of the apply stages (events inside the captured step)
         a4_span_ms = sch.timing_span(pos.POS_SCHEME_SFB) if has_fc else None
         ps_span_ms = sch.timing_span(pos.POS_SCHEME_PS) if has_dense else None
-    else:
+        unit_apply_ms = [sch.timing(un["layers"][0])[2] for un in units]
+    timeline = sch.timeline(len(units)) if a.layers else None
+    unit_times = [sch.timing(un["layers"][0]) for un in units] if a.layers else None
+    if not a.no_trace:   # the same step, traced, replayed as often as the timed region
+        sch.set_trace(True)
+        if a.eager:
+            run_t = lambda i: step(main)
+        else:
+            graphs_t = capture_ring(step, main)
+            run_t = lambda i: graphs_t[i % len(graphs_t)].replay()
+        for i in range(4):
+            run_t(i)
+        refresh_grads()
+        torch.cuda.synchronize()
+        sch.trace_reset()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(main)
+        for i in range(a.steps):
+            run_t(i)
+        r1.record(main)
+        torch.cuda.synchronize()
+        traced_ms = r0.elapsed_time(r1) / a.steps
         a4_span_ms = sch.trace_span(pos.POS_SCHEME_SFB)[0] / 1e3 if has_fc else None
         ps_span_ms = sch.trace_span(pos.POS_SCHEME_PS)[0] / 1e3 if has_dense else None
-    timeline = sch.timeline(len(units)) if a.layers else None
-    unit_apply_ms = [(sch.timing(un["layers"][0])[2] if a.no_trace else sch.trace(un["layers"][0])[0] / 1e3)
-                     for un in units]
-    unit_times = [sch.timing(un["layers"][0]) for un in units] if a.layers else None
+        unit_apply_ms = [sch.trace(un["layers"][0])[0] / 1e3 for un in units]
+        if world > 1:
+            t = torch.tensor([traced_ms, a4_span_ms or 0.0, ps_span_ms or 0.0] + unit_apply_ms, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            v = t.tolist()
+            traced_ms = v[0]
+            a4_span_ms = v[1] if has_fc else None
+            ps_span_ms = v[2] if has_dense else None
+            unit_apply_ms = v[3:]
+        graphs_t = None
+        sch.set_trace(False)
     # clock soak: if the timed region was too short for the 50 ms sampler, keep the same load
     # running (untimed) for ~1 s so the clock record describes this workload under load
     soak_t0 = soak_t1 = None
@@ -695,10 +725,12 @@ def run_ours(a):
             "traffic": traffic,
             "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
             "kernel_ms_note": "device-side trace (%%globaltimer stamped by the kernels, no events in "
-                              "the captured step), averaged over the timed steps: span from the first "
+                              "the captured step) of a replay of the same step right after the "
+                              "(untraced) timed region, as many steps, averaged: span from the first "
                               "reconstruction CTA's start to the last one's end in a step (consecutive "
                               "layers' reconstructions overlap on two streams); sum of per-layer "
                               "durations: %.4f ms" % a4_ms_sum,
+            "traced_ms_per_step": traced_ms,
             "per_layer_ms": {model.layers[un["layers"][0]].name: unit_apply_ms[i]
                              for i, un in enumerate(units) if un["kind"] == "fc"},
             "peak_source": peaks["source"],

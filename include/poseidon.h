@@ -356,6 +356,11 @@ int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, in
  * the scheme has no traced kernels (e.g. the SIMT f32 path). */
 int pos_sched_trace_span(pos_sched* s, int32_t scheme, double* avg_us, int64_t* steps);
 int pos_sched_trace_reset(pos_sched* s);
+/* Turn device-side tracing on / off for the iterations issued from now on (between iterations
+ * only, else POS_ESTATE). CUDA graphs captured earlier keep the setting they were captured with.
+ * Lets a caller time steps untraced and take kernel durations from separately traced steps. The
+ * records (pos_sched_trace*) stay readable after tracing is turned off again. */
+int pos_sched_set_trace(pos_sched* s, int32_t on);
 /* With POS_SCHED_TIMING(_APPLY): the device-time SPAN (earliest apply start to latest apply end)
  * of all units of `scheme` (POS_SCHEME_SFB or POS_SCHEME_PS) within one iteration, averaged over
  * the (up to 4) most recent iterations whose timing events are still live. Reconstructions of

@@ -411,6 +411,10 @@ class Scheduler:
     def trace_reset(self):
         _chk(lib().pos_sched_trace_reset(self.h), "pos_sched_trace_reset")
 
+    def set_trace(self, on):
+        """pos_sched_set_trace: device-side tracing on / off for the iterations issued from now on."""
+        _chk(lib().pos_sched_set_trace(self.h, 1 if on else 0), "pos_sched_set_trace")
+
     def timing_reset(self):
         _chk(lib().pos_sched_timing_reset(self.h), "pos_sched_timing_reset")
 

@@ -765,7 +765,7 @@ int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, in
   clear_error();
   int rc = check_layer(s, l);
   if (rc) return rc;
-  if (!tracing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TRACE");
+  if (!tracing(s) && s->traced_ctas == -2) POS_FAIL(POS_ESTATE, "tracing was never on (POS_SCHED_TRACE / pos_sched_set_trace)");
   if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
   const Unit& un = s->units[s->layers[l].unit];
   if (!un.trace) POS_FAIL(POS_ESTATE, "no traced iteration yet");
@@ -776,7 +776,7 @@ int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, in
 int pos_sched_trace_span(pos_sched* s, int32_t scheme, double* avg_us, int64_t* steps) {
   clear_error();
   POS_CHECK_ARG(s && (scheme == POS_SCHEME_SFB || scheme == POS_SCHEME_PS), "bad arguments");
-  if (!tracing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TRACE");
+  if (!tracing(s) && s->traced_ctas == -2) POS_FAIL(POS_ESTATE, "tracing was never on (POS_SCHED_TRACE / pos_sched_set_trace)");
   const int k = scheme == POS_SCHEME_SFB ? 1 : 0;
   if (!s->group[k] || s->group_expected[k] == 0)
     POS_FAIL(POS_ESTATE, "no traced group for scheme %d (no units, or an untraced SIMT path)", scheme);
@@ -787,12 +787,27 @@ int pos_sched_trace_span(pos_sched* s, int32_t scheme, double* avg_us, int64_t* 
 int pos_sched_trace_reset(pos_sched* s) {
   clear_error();
   POS_CHECK_ARG(s, "bad arguments");
-  if (!tracing(s)) POS_FAIL(POS_ESTATE, "scheduler created without POS_SCHED_TRACE");
+  if (!tracing(s) && s->traced_ctas == -2) POS_FAIL(POS_ESTATE, "tracing was never on (POS_SCHED_TRACE / pos_sched_set_trace)");
   POS_CUDA_TRY(cudaDeviceSynchronize());
   for (auto& un : s->units)
     if (un.trace) POS_CUDA_TRY(ktrace_reset(un.trace));
   for (auto* g : s->group)
     if (g) POS_CUDA_TRY(ktrace_reset(g));
+  return POS_OK;
+}
+
+int pos_sched_set_trace(pos_sched* s, int32_t on) {
+  clear_error();
+  POS_CHECK_ARG(s, "bad arguments");
+  if (s->in_iter) POS_FAIL(POS_ESTATE, "pos_sched_set_trace inside an iteration");
+  if (on) {
+    s->flags |= POS_SCHED_TRACE;
+    // allocate / re-arm the records now: iteration begin may run under CUDA-graph stream capture
+    int rc = prepare_tracing(s);
+    if (rc) return rc;
+  } else {
+    s->flags &= ~POS_SCHED_TRACE;
+  }
   return POS_OK;
 }
 

@@ -55,10 +55,12 @@ constexpr int BN = POS_SFB_BN;      // tile cols (n) = UMMA N = TMEM columns per
 #ifndef POS_SFB_WSLOTS
 #define POS_SFB_WSLOTS 5
 #endif
+#ifndef POS_SFB_PWSLOTS
+#define POS_SFB_PWSLOTS 5
+#endif
 // The kernel is bound by the W read-modify-write (8 B per element): shared memory goes to W
 // prefetch depth (WSLOTS x 16 KB in flight per SM) rather than to operand stages (K*P is small).
 constexpr int STAGES = POS_SFB_STAGES;   // operand ring depth
-constexpr int WSLOTS = POS_SFB_WSLOTS;   // W sub-tile ring depth
 constexpr int WSUB = 32;            // W sub-tile columns (32 fp32 = one 128-byte swizzle row)
 constexpr int NSUB = BN / WSUB;     // sub-tiles per tile
 constexpr int SWZ = 128;            // swizzle span in bytes (one operand "row" chunk)
@@ -72,6 +74,19 @@ constexpr int TR = 4;               // tile-index ring depth (dynamic tile sched
 #ifndef POS_SFB_PSTAGES
 #define POS_SFB_PSTAGES 4
 #endif
+// Diagnostics only (never in the shipped build): 1 = no W traffic in the epilogue, 2 = no MMAs,
+// 3 = no MMAs and no operand loads.
+#ifndef POS_SFB_EXP
+#define POS_SFB_EXP 0
+#endif
+#ifndef POS_SFB_EPI
+#define POS_SFB_EPI 1
+#endif
+#ifndef POS_SFB_PEPI
+#define POS_SFB_PEPI 1
+#endif
+// Epilogue warpgroups (per variant): each owns every EPI-th W sub-tile of the CTA's global
+// sub-tile sequence, so one group's TMEM load / smem update overlaps the other's barrier + store.
 // Shared-memory layout of one CTA. kPair: CTA-pair kernel (tcgen05 cta_group::2): the pair
 // computes a 256 x BN tile, each CTA holds its 128 rows of U and HALF of the tile's V columns,
 // so a stage is 2/3 the size and more stages fit — the large-K*P shapes are bound by operand
@@ -82,27 +97,24 @@ struct Lay {
   static constexpr int kBCols = kPair ? BN / 2 : BN;          // V columns held per CTA
   static constexpr int kBBytes = KBYTES * kBCols;
   static constexpr int kStageBytes = A_BYTES + kBBytes;
-  static constexpr int kData = kStages * kStageBytes + WSLOTS * W_BYTES;
-  static constexpr int kBars = 8 * (2 * kStages + 2 * WSLOTS + 4 + 2 * TR) + 16 + 4 * TR;
+  static constexpr int kWSlots = kPair ? POS_SFB_PWSLOTS : POS_SFB_WSLOTS;   // W sub-tile ring depth
+  static constexpr int kEpi = kPair ? POS_SFB_PEPI : POS_SFB_EPI;             // epilogue warpgroups
+  static constexpr int kThreads = 128 + 128 * kEpi;
+  static constexpr int kData = kStages * kStageBytes + kWSlots * W_BYTES;
+  static constexpr int kBars = 8 * (2 * kStages + 2 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
   static constexpr int kTotal = kData + kBars + 1024;         // + alignment slack
   static constexpr int kTileRows = kPair ? 2 * BM : BM;       // W rows per tile
 };
 constexpr int STAGE_BYTES = Lay<false>::kStageBytes;
 constexpr int SMEM_TOTAL = Lay<false>::kTotal;
-#ifndef POS_SFB_EPI
-#define POS_SFB_EPI 1
-#endif
-// Epilogue warpgroups: each owns every EPI-th W sub-tile of the CTA's global sub-tile sequence,
-// so one group's TMEM load / smem update overlaps the other's barrier + TMA store.
-constexpr int EPI = POS_SFB_EPI;
-constexpr int THREADS = 128 + 128 * EPI;
 constexpr int TMEM_COLS = 2 * BN;
 
 static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 static_assert(Lay<true>::kTotal <= 232448, "shared memory budget (CTA pair)");
 // A W slot must always be consumed by the same epilogue group: a group waits on a slot's full
 // barrier by phase parity, which is only sound if it consumed the slot's previous phase itself.
-static_assert(WSLOTS % EPI == 0, "W slots must be a multiple of the epilogue groups");
+static_assert(Lay<false>::kWSlots % Lay<false>::kEpi == 0 && Lay<true>::kWSlots % Lay<true>::kEpi == 0,
+              "W slots must be a multiple of the epilogue groups");
 
 // ------------------------------------------------------------------------------------ PTX ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -339,7 +351,7 @@ struct TileInfo {
 };
 
 template <bool kTF32, bool kPair>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Lay<kPair>::kThreads, 1)
 sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA2,
               const __grid_constant__ CUtensorMap tmB2, TileInfo ti, float alpha, int accumulate) {
@@ -351,6 +363,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   constexpr int UK = 32 / EB;                // UMMA K (16 bf16 / 8 tf32)
   constexpr int BOX_BYTES = BK * SWZ;        // one TMA box: BK rows x 128 B
   constexpr uint32_t IDESC = instr_desc<kTF32, kPair>();
+  constexpr int WSLOTS = L::kWSlots, EPI = L::kEpi;
   // epilogue warps that must drain an accumulator before the MMA may overwrite it
   constexpr int kDrainers = 4 * EPI * (kPair ? 2 : 1);
   // tile-ring consumers: (MMA issuer | peer operand producer) + W producer + epilogue, per CTA
@@ -481,7 +494,9 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           mbar_wait(b_empty + 8 * stage, phase ^ 1);
           const uint32_t sA = sbase + stage * L::kStageBytes, sB = sA + A_BYTES;
           const int k0 = kb * BK;
-          if constexpr (kPair) {
+          if (POS_SFB_EXP == 3) {   // diagnostic: no operand traffic (and no MMAs)
+            if (!kPair || leader) mbar_arrive(b_full + 8 * stage);
+          } else if constexpr (kPair) {
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t full = map_rank(b_full + 8 * stage, 0);
             if (leader) mbar_expect_tx(b_full + 8 * stage, 2 * L::kStageBytes);
@@ -526,7 +541,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           for (int kk = 0; kk < BK / UK; ++kk) {
             const uint64_t ad = smem_desc<kTF32>(sA + kk * UK * SWZ, BOX_BYTES);
             const uint64_t bd = smem_desc<kTF32>(sB + kk * UK * SWZ, BOX_BYTES);
-            umma<kTF32, kPair>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+            if (POS_SFB_EXP != 2 && POS_SFB_EXP != 3) umma<kTF32, kPair>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
           }
           umma_commit<kPair>(b_empty + 8 * stage);   // frees the smem stage(s) when done
           if (++stage == ST) { stage = 0; phase ^= 1; }
@@ -548,7 +563,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (int j = 0; j < nsub; ++j) {
           mbar_wait(b_wempty + 8 * ws, wphase ^ 1);
           const uint32_t wf = b_wfull + 8 * ws;
-          if (accumulate) {
+          if (accumulate && POS_SFB_EXP != 1) {
             mbar_expect_tx(wf, W_BYTES);
             if (POS_SFB_L2HINT)
               tma_load_2d_hint(&tmW, wf, sW0 + ws * W_BYTES, n0 + j * WSUB, m0, policy_evict_first());
@@ -614,6 +629,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         tmem_ld32(tmem_base + lane_addr + acc * BN + j * WSUB, r);
         if (j == jlast) release_acc(acc);     // accumulator fully drained by this thread
         mbar_wait(b_wfull + 8 * ws, wphase);
+        if (POS_SFB_EXP == 1) {   // diagnostic: no W traffic (TMEM drained, slot recycled)
+          named_bar_sync(1 + g, 128);
+          if (et == 0) mbar_arrive(b_wempty + 8 * ws);
+          continue;
+        }
         const uint32_t row = sW0 + ws * W_BYTES + et * SWZ;
         float4 w[8];
 #pragma unroll
@@ -741,7 +761,7 @@ int max_pairs() {
     if (set_smem_attr<kTF32, true>() == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(2 * (unsigned)num_sms());
-      cfg.blockDim = dim3(THREADS);
+      cfg.blockDim = dim3(Lay<true>::kThreads);
       cfg.dynamicSmemBytes = Lay<true>::kTotal;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -832,7 +852,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   if constexpr (kPair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.grid);
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(Lay<true>::kThreads);
     cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -845,7 +865,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
     return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true>, pl.tmA, pl.tmB, pl.tmW, pl.tmA2,
                               pl.tmB2, ti, alpha, accumulate);
   } else {
-    sfb_tc_kernel<kTF32, false><<<pl.grid, THREADS, smem_bytes, s>>>(
+    sfb_tc_kernel<kTF32, false><<<pl.grid, Lay<false>::kThreads, smem_bytes, s>>>(
         pl.tmA, pl.tmB, pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
     return cudaGetLastError();
   }

@@ -526,3 +526,79 @@ def test_sched_device_trace():
     g = None
     sch.close()
     ctx.close()
+
+
+@pytest.mark.gpu
+def test_sched_set_trace_toggle_under_capture():
+    """pos_sched_set_trace: a scheduler created untraced runs (eager and captured) iterations, then
+    tracing is switched on and the FIRST traced iteration is captured into a CUDA graph (the trace
+    records are allocated by set_trace, outside the capture); only the traced replays are counted,
+    and the results match the oracle bitwise throughout."""
+    model = make_model(6)
+    a = si.EXACT_ALPHA
+    ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
+    sch = pos.Scheduler(ctx, len(model), trace=False)
+    dev = []
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            n = d["n"]
+            W = torch.zeros(pos.pos_padded_size(n, 1), device="cuda"); W[:n] = to_dev(d["W"])
+            G = torch.zeros_like(W); G[:n] = to_dev(d["g"])
+            sch.add_dense(l, n, W, G)
+            dev.append({"W": W, "G": G})
+        else:
+            W, b = to_dev(d["W"]), to_dev(d["b"])
+            sch.add_fc(l, d["M"], d["N"], d["K"], W, b, None, "bf16", pos.POS_IN_BF16)
+            dev.append({"W": W, "b": b, "u": to_dev(d["u"], "bf16"), "v": to_dev(d["v"], "bf16")})
+
+    def step(stream):
+        sch.begin(a)
+        for l in reversed(range(len(model))):
+            if model[l]["kind"] == "dense":
+                sch.grad_ready(l, stream)
+            else:
+                sch.factors_ready(l, dev[l]["u"], dev[l]["v"], stream)
+        sch.end(stream)
+
+    def capture():
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+            step(torch.cuda.current_stream())
+        torch.cuda.current_stream().wait_stream(cs)
+        return g
+
+    step(torch.cuda.current_stream())               # untraced, eager
+    g0 = capture()                                  # untraced, captured
+    g0.replay()
+    torch.cuda.synchronize()
+    with pytest.raises(pos.PoseidonError):
+        sch.trace(0)                                # not tracing
+    sch.set_trace(True)
+    g1 = capture()                                  # first traced iteration: under capture
+    g1.replay()
+    g1.replay()
+    torch.cuda.synchronize()
+    for l in range(len(model)):
+        avg, last, n = sch.trace(l)
+        assert n == 2 and avg > 0 and last > 0, (l, avg, last, n)
+    assert sch.trace_span(pos.POS_SCHEME_SFB)[1] == 2
+    sch.set_trace(False)
+    g0.replay()                                     # the untraced graph still runs untraced
+    torch.cuda.synchronize()
+    assert sch.trace(0)[2] == 2
+    iters = 5   # eager + g0 replay + g1 x 2 + g0 replay (a capture does not execute)
+    for l, d in enumerate(model):
+        if d["kind"] == "dense":
+            r = d["W"]
+            for _ in range(iters):
+                r = sync.ps_update(r, [d["g"]], a)
+            assert np.array_equal(to_host(dev[l]["W"][:d["n"]]), r)
+        else:
+            Wr, br = d["W"], d["b"]
+            for _ in range(iters):
+                Wr, br = sync.sfb_update(Wr, br, [d["u"]], [d["v"]], a)
+            assert np.array_equal(to_host(dev[l]["W"]), Wr) and np.array_equal(to_host(dev[l]["b"]), br)
+    sch.close()
+    ctx.close()
