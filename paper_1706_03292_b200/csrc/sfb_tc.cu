@@ -103,7 +103,6 @@ struct Lay {
   static constexpr int kData = kStages * kStageBytes + kWSlots * W_BYTES;
   static constexpr int kBars = 8 * (2 * kStages + 2 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
   static constexpr int kTotal = kData + kBars + 1024;         // + alignment slack
-  static constexpr int kTileRows = kPair ? 2 * BM : BM;       // W rows per tile
 };
 constexpr int STAGE_BYTES = Lay<false>::kStageBytes;
 constexpr int SMEM_TOTAL = Lay<false>::kTotal;
@@ -219,11 +218,11 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t adesc, uint64_t b
 // mbarrier arrives when all previously issued tcgen05 ops of this thread have completed
 // (kPair: on the barrier at this offset in BOTH CTAs of the pair)
 template <bool kPair>
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
+__device__ __forceinline__ void umma_commit(uint32_t bar, uint16_t mask = 0x3) {
   if constexpr (kPair) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(bar), "h"((uint16_t)0x3)
+        " [%0], %1;" ::"r"(bar), "h"(mask)
         : "memory");
   } else {
     asm volatile(
@@ -289,6 +288,17 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
       : "memory");
 }
+// Same, multicast: the box lands at `dst` in every CTA of `mask`; each destination's bytes complete
+// on the barrier at the same offset in the leader (even CTA) of the destination's pair
+__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap* map, uint32_t leader_bar,
+                                                    uint32_t dst, int32_t c0, int32_t c1,
+                                                    uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -350,7 +360,11 @@ struct TileInfo {
   KTrace trace, group;    // device-side launch trace (off when rec == nullptr)
 };
 
-template <bool kTF32, bool kPair>
+// kMc (with kPair): cluster of 4 = two CTA pairs stacked along m (a 512 x BN tile); both pairs
+// need the same V columns, so each V box is loaded once and multicast to the two CTAs that hold it
+// — 1/4 less operand traffic through L2 than two independent pairs (the large-K*P shapes are bound
+// by L2 -> SM operand bytes).
+template <bool kTF32, bool kPair, bool kMc = false>
 __global__ void __launch_bounds__(Lay<kPair>::kThreads, 1)
 sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA2,
@@ -365,9 +379,13 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   constexpr uint32_t IDESC = instr_desc<kTF32, kPair>();
   constexpr int WSLOTS = L::kWSlots, EPI = L::kEpi;
   // epilogue warps that must drain an accumulator before the MMA may overwrite it
+  static_assert(!kMc || kPair, "multicast clusters are made of CTA pairs");
+  constexpr int kCl = kMc ? 4 : (kPair ? 2 : 1);   // CTAs per cluster (scheduling unit)
+  constexpr int kTileRows = kCl * BM;               // W rows per (cluster) tile
   constexpr int kDrainers = 4 * EPI * (kPair ? 2 : 1);
   // tile-ring consumers: (MMA issuer | peer operand producer) + W producer + epilogue, per CTA
-  constexpr int kRingConsumers = (2 + 128 * EPI) * (kPair ? 2 : 1);
+  // (kMc: the second pair's leader is both an MMA issuer and a ring-reading operand producer)
+  constexpr int kRingConsumers = (2 + 128 * EPI) * kCl + (kMc ? 1 : 0);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -385,7 +403,9 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   // CTA pair: the even CTA (rank 0) fetches tiles, issues the MMAs and owns the shared
   // barriers (full, tempty, rempty); each CTA loads and updates its own 128 rows.
   const uint32_t crank = kPair ? cluster_rank() : 0;
-  const bool leader = crank == 0;
+  const uint32_t prank = crank & 1u, pbase = crank & ~1u;   // rank within the pair, pair leader
+  const bool leader = prank == 0;                           // pair leader: issues the MMAs
+  const bool fetcher = crank == 0;                          // cluster leader: fetches the tiles
   const int unit = kPair ? (int)cluster_id_x() : (int)blockIdx.x;   // scheduling unit
   const int nunits = kPair ? (int)nclusters_x() : (int)gridDim.x;
   auto wait_ring = [&](uint32_t bar, uint32_t parity) {
@@ -412,7 +432,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   ktrace_begin(ti.group);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < ST; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, 1); }
+    // kMc: a stage is free only when BOTH pairs' MMAs have read it (its V boxes were multicast)
+    for (int i = 0; i < ST; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, kMc ? 2 : 1); }
     for (int i = 0; i < WSLOTS; ++i) { mbar_init(b_wfull + 8 * i, 1); mbar_init(b_wempty + 8 * i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(b_tfull + 8 * i, 1);
@@ -463,7 +484,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (!dyn) {
           t = unit + it * nunits;
           if (t >= ti.num_tiles) break;
-        } else if (kPair && !leader) {
+        } else if (kPair && !fetcher) {
           t = tile_of(it, rphase);
           if (t < 0) break;
         } else {   // fetch the next tile and publish it to the other roles (and the peer CTA)
@@ -473,8 +494,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           if (t >= ti.num_tiles) t = -1;
           tile_ring[slot] = t;
           if constexpr (kPair) {
-            st_cluster_u32(map_rank(smem_u32((const void*)&tile_ring[slot]), 1), (uint32_t)t);
-            mbar_arrive_cluster(map_rank(b_rfull + 8 * slot, 1));
+#pragma unroll
+            for (int q = 1; q < kCl; ++q) {
+              st_cluster_u32(map_rank(smem_u32((const void*)&tile_ring[slot]), q), (uint32_t)t);
+              mbar_arrive_cluster(map_rank(b_rfull + 8 * slot, q));
+            }
           }
           mbar_arrive(b_rfull + 8 * slot);
           if (slot == TR - 1) rphase ^= 1;
@@ -488,8 +512,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             break;
           }
         }
-        const int m0 = (t / ti.nb_n) * L::kTileRows + (int)crank * BM;
-        const int nb0 = (t % ti.nb_n) * BN + (int)crank * L::kBCols;   // this CTA's V columns
+        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM;
+        const int nb0 = (t % ti.nb_n) * BN + (int)prank * L::kBCols;   // this CTA's V columns
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(b_empty + 8 * stage, phase ^ 1);
           const uint32_t sA = sbase + stage * L::kStageBytes, sB = sA + A_BYTES;
@@ -497,15 +521,24 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           if (POS_SFB_EXP == 3) {   // diagnostic: no operand traffic (and no MMAs)
             if (!kPair || leader) mbar_arrive(b_full + 8 * stage);
           } else if constexpr (kPair) {
-            // both CTAs' bytes complete on the leader's full barrier
-            const uint32_t full = map_rank(b_full + 8 * stage, 0);
+            // both CTAs' bytes complete on the pair leader's full barrier
+            const uint32_t full = map_rank(b_full + 8 * stage, pbase);
             if (leader) mbar_expect_tx(b_full + 8 * stage, 2 * L::kStageBytes);
 #pragma unroll
             for (int c = 0; c < BM / CHUNK; ++c)
               tma_load_2d_pair(mA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
+            if constexpr (kMc) {
+              // V boxes: CTA r of pair p loads the boxes c = p (mod 2) of its column half, for
+              // itself and for CTA r of the other pair
+              const uint16_t mask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
 #pragma unroll
-            for (int c = 0; c < L::kBCols / CHUNK; ++c)
-              tma_load_2d_pair(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
+              for (int c = (int)(crank >> 1); c < L::kBCols / CHUNK; c += 2)
+                tma_load_2d_pair_mc(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0, mask);
+            } else {
+#pragma unroll
+              for (int c = 0; c < L::kBCols / CHUNK; ++c)
+                tma_load_2d_pair(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
+            }
           } else {
             const uint32_t full = b_full + 8 * stage;
             mbar_expect_tx(full, L::kStageBytes);
@@ -543,10 +576,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint64_t bd = smem_desc<kTF32>(sB + kk * UK * SWZ, BOX_BYTES);
             if (POS_SFB_EXP != 2 && POS_SFB_EXP != 3) umma<kTF32, kPair>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
           }
-          umma_commit<kPair>(b_empty + 8 * stage);   // frees the smem stage(s) when done
+          // frees the smem stage(s) when done (kMc: in all four CTAs — the V boxes are shared)
+          umma_commit<kPair>(b_empty + 8 * stage, kMc ? 0xF : 0x3);
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
-        umma_commit<kPair>(b_tfull + 8 * acc);        // accumulator ready for the epilogue(s)
+        umma_commit<kPair>(b_tfull + 8 * acc, (uint16_t)(0x3u << pbase));   // accumulator ready
         if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     }
@@ -558,7 +592,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int it = 0;; ++it) {
         const int t = tile_of(it, rphase);
         if (t < 0) break;
-        const int m0 = (t / ti.nb_n) * L::kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
+        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
         const int nsub = nsub_of(ti.N, n0);
         for (int j = 0; j < nsub; ++j) {
           mbar_wait(b_wempty + 8 * ws, wphase ^ 1);
@@ -592,14 +626,14 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (kPair) mbar_arrive_remote(map_rank(b_tempty + 8 * a, 0));
+        if constexpr (kPair) mbar_arrive_remote(map_rank(b_tempty + 8 * a, pbase));
         else mbar_arrive(b_tempty + 8 * a);
       }
     };
     for (int it = 0;; ++it) {
       const int t = tile_of(it, rphase);
       if (t < 0) break;
-      const int m0 = (t / ti.nb_n) * L::kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
+      const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
       const int nsub = nsub_of(ti.N, n0);
       // this group's sub-tiles of the tile: j = j0, j0 + EPI, ...; the last one frees TMEM
       const int j0 = (int)((g - (int)(sseq % EPI) + EPI) % EPI);
@@ -735,6 +769,21 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 #endif
 // CTA-pair kernel for K*P >= POS_SFB_PAIR_KP (env POS_SFB_PAIR=0|1 forces it off / on,
 // POS_SFB_PAIR_KP overrides the threshold; read at plan time).
+#ifndef POS_SFB_MC_KP
+#define POS_SFB_MC_KP (1LL << 40)   // off until measured (POS_SFB_MC=1 turns it on)
+#endif
+// 4-CTA multicast kernel (two pairs sharing the V boxes) for K*P >= POS_SFB_MC_KP among the pair
+// shapes (env POS_SFB_MC=0|1 forces it off / on; POS_SFB_MC_KP overrides the threshold).
+bool use_mc(int64_t KP) {
+  if (const char* f = getenv("POS_SFB_MC")) {
+    if (f[0] == '0') return false;
+    if (f[0] == '1') return true;
+  }
+  int64_t thr = POS_SFB_MC_KP;
+  if (const char* e = getenv("POS_SFB_MC_KP")) thr = atoll(e);
+  return KP >= thr;
+}
+
 bool use_pair(int64_t KP) {
   if (const char* f = getenv("POS_SFB_PAIR")) {
     if (f[0] == '0') return false;
@@ -745,43 +794,48 @@ bool use_pair(int64_t KP) {
   return KP >= thr;
 }
 
-template <bool kTF32, bool kPair>
+template <bool kTF32, bool kPair, bool kMc = false>
 cudaError_t set_smem_attr() {
-  static cudaError_t e = cudaFuncSetAttribute(
-      sfb_tc_kernel<kTF32, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<kPair>::kTotal);
+  static cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32, kPair, kMc>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              Lay<kPair>::kTotal);
   return e;
 }
 
-// Co-resident CTA pairs of the pair kernel on this device (0 = cannot launch as clusters)
-template <bool kTF32>
-int max_pairs() {
+// Co-resident clusters of the pair kernel (kMc: of the 4-CTA multicast kernel) on this device
+// (0 = cannot launch as clusters)
+template <bool kTF32, bool kMc>
+int max_clusters() {
   static int n = -1;
+  constexpr unsigned kCl = kMc ? 4 : 2;
   if (n < 0) {
     n = 0;
-    if (set_smem_attr<kTF32, true>() == cudaSuccess) {
+    if (set_smem_attr<kTF32, true, kMc>() == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(2 * (unsigned)num_sms());
+      cfg.gridDim = dim3(kCl * (unsigned)num_sms());
       cfg.blockDim = dim3(Lay<true>::kThreads);
       cfg.dynamicSmemBytes = Lay<true>::kTotal;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.x = kCl;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int c = 0;
-      if (cudaOccupancyMaxActiveClusters(&c, sfb_tc_kernel<kTF32, true>, &cfg) == cudaSuccess)
+      if (cudaOccupancyMaxActiveClusters(&c, sfb_tc_kernel<kTF32, true, kMc>, &cfg) == cudaSuccess)
         n = c;
       else
         clear_stale_launch_error();
     }
     if (getenv("POS_SFB_VERBOSE"))
-      fprintf(stderr, "[poseidon] sfb_tc pair kernel: %d co-resident CTA pairs (%d SMs)\n", n,
-              num_sms());
+      fprintf(stderr, "[poseidon] sfb_tc %s kernel: %d co-resident clusters of %u (%d SMs)\n",
+              kMc ? "multicast" : "pair", n, kCl, num_sms());
   }
   return n;
 }
+template <bool kTF32>
+int max_pairs() { return max_clusters<kTF32, false>(); }
 
 template <bool kTF32>
 bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
@@ -823,23 +877,27 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
   int ctas = num_sms();
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
   pl->pair = use_pair(KP) && ctas >= 2 && max_pairs<kTF32>() > 0;
-  const int64_t rows = pl->pair ? 2 * BM : BM;
+  pl->mc = pl->pair && use_mc(KP) && ctas >= 4 && max_clusters<kTF32, true>() > 0;
+  const int cl = pl->mc ? 4 : (pl->pair ? 2 : 1);   // CTAs per scheduling unit
+  const int64_t rows = (int64_t)cl * BM;
   const int64_t tiles = (int64_t)pl->nb_n * ((M + rows - 1) / rows);
   if (tiles > INT32_MAX) return false;
   pl->num_tiles = (int)tiles;
-  // persistent CTAs, or CTA pairs — no more pairs than can be co-resident (a TPC with one
-  // usable SM cannot host a pair; a pair that waits for a second wave would be a straggler)
-  int units = pl->pair ? std::min(ctas / 2, max_pairs<kTF32>()) : ctas;
+  // persistent CTAs, or clusters — no more clusters than can be co-resident (a TPC with one
+  // usable SM cannot host a pair; a cluster that waits for a second wave would be a straggler)
+  int units = ctas;
+  if (pl->mc) units = std::min(ctas / 4, max_clusters<kTF32, true>());
+  else if (pl->pair) units = std::min(ctas / 2, max_pairs<kTF32>());
   if (units > pl->num_tiles) units = pl->num_tiles;
-  pl->grid = pl->pair ? 2 * units : units;
+  pl->grid = cl * units;
   return true;
 }
 
-template <bool kTF32, bool kPair>
+template <bool kTF32, bool kPair, bool kMc = false>
 cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
   clear_stale_launch_error();
   constexpr int smem_bytes = Lay<kPair>::kTotal;
-  if (cudaError_t e = set_smem_attr<kTF32, kPair>(); e != cudaSuccess) return e;
+  if (cudaError_t e = set_smem_attr<kTF32, kPair, kMc>(); e != cudaSuccess) return e;
   TileInfo ti;
   ti.M = pl.M; ti.N = pl.N; ti.KP = pl.KP;
   ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
@@ -857,13 +915,13 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;   // the CTA pair shares one TPC
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = kMc ? 4 : 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true>, pl.tmA, pl.tmB, pl.tmW, pl.tmA2,
-                              pl.tmB2, ti, alpha, accumulate);
+    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true, kMc>, pl.tmA, pl.tmB, pl.tmW,
+                              pl.tmA2, pl.tmB2, ti, alpha, accumulate);
   } else {
     sfb_tc_kernel<kTF32, false><<<pl.grid, Lay<false>::kThreads, smem_bytes, s>>>(
         pl.tmA, pl.tmB, pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
@@ -893,6 +951,9 @@ bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t d
 }
 
 cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
+  if (pl.mc)
+    return pl.tf32 ? launch_plan_impl<true, true, true>(pl, alpha, accumulate, s)
+                   : launch_plan_impl<false, true, true>(pl, alpha, accumulate, s);
   if (pl.pair)
     return pl.tf32 ? launch_plan_impl<true, true>(pl, alpha, accumulate, s)
                    : launch_plan_impl<false, true>(pl, alpha, accumulate, s);

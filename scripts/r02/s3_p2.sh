@@ -19,6 +19,7 @@ for i in 1 2 3; do
     POS_NVLS_CTAS=16 POS_SFB_PAIR=1 timeout 300 $T --master-port $port bench.py --gpus $N --steps 30 --warmup 5 --config $cfg --no-cpu-baseline --no-e2e --no-tf32 > $O/stress_${cfg}_$i.json 2> $O/stress_${cfg}_$i.err; echo "stress $cfg $i rc=$?" >> $O/stress.log
   done
 done
-tail -n 2 $O/pytest_multi.log $O/nvlink.log
+timeout 600 $T --master-port 29599 scripts/scheme_crossover.py $O/scheme_crossover.json > $O/crossover.log 2>&1; echo "xover rc=$?" >> $O/crossover.log
+tail -n 2 $O/pytest_multi.log $O/nvlink.log $O/crossover.log
 cat $O/stress.log
 for cfg in c3 c1 c2 c4; do python -c "import json; d=json.loads(open('$O/bench_$cfg.json').read().strip().splitlines()[-1]); print('$cfg', round(d['ms_per_step'],4), round(d['roofline']['step']['frac_pipelined'],3), d['clocks'])" 2>&1 | tail -1; done
