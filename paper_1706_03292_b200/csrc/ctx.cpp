@@ -162,7 +162,11 @@ static int ctx_common_init(pos_ctx* c) {
   POS_CUDA_TRY(cudaGetDevice(&c->device));
   int lo = 0, hi = 0;
   POS_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+  // comm stream priority: the greatest by default; POS_COMM_PRIO=n sets lo + n (clamped), an
+  // experiment knob for the order in which pending PS / pack CTAs get SMs
+  int prio = hi;
+  if (const char* e = getenv("POS_COMM_PRIO")) prio = std::max(hi, std::min(lo, lo - atoi(e)));
+  POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio));
   // watchdog error word: host-mapped, so the host reads it without synchronising
   int* h = nullptr;
   POS_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h), sizeof(int), cudaHostAllocMapped));

@@ -30,7 +30,8 @@
 
 namespace {
 
-constexpr int kPool = 5;    // apply streams: [0], [4] reconstructions; [1..3] dense applies
+constexpr int kPool = 6;    // apply streams: [0], [4] reconstructions; [1..3] dense applies;
+                             // [5] flag-mode factor packs (high priority)
 constexpr int kTRing = 4;   // timing event sets per unit (iterations in flight)
 
 struct TSlot {
@@ -103,6 +104,7 @@ struct pos_sched {
   int last_sfb = -1;       // most recently issued SFB unit of this iteration
   bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
   int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1: one, in order)
+  bool pack_stream = true;    // flag-mode packs on their own stream (POS_PACK_STREAM=0: comm stream)
   int n_sfb = 0;              // SFB units registered
   bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
   // POS_SCHED_TRACE: one group record per scheme (all of a step's PS / SFB apply kernels)
@@ -246,6 +248,10 @@ int issue_unit(pos_sched* s, int ui) {
   // first stage: the comm stream when a collective follows; else an auxiliary apply stream, so the
   // factor pack of the next SFB layer overlaps the reconstruction of this one
   cudaStream_t cs = coll ? c->comm_stream : s->pool[1 + un.seq % 3];
+  // Flag-mode packs (multicast stores + ready flags, no cross-GPU barrier) need no ordering with
+  // the fused PS kernels, which keep the comm stream to themselves: the PS chain then starts
+  // with the first dense unit instead of queueing behind every factor pack of the step
+  if (coll && un.scheme == POS_SCHEME_SFB && un.flag_mode && s->pack_stream) cs = s->pool[5];
   for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_in, 0));
   // the stage that WRITES W waits for b^l to have finished reading it (WAR)
   const Layer& l0 = s->layers[un.members[0]];
@@ -419,12 +425,13 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   s->flags = flags;
   s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
   if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = atoi(e) > 1 ? 2 : 1;
+  if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] != '0';
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   for (int i = 0; i < kPool; ++i) {
-    cudaError_t e = cudaStreamCreateWithPriority(&s->pool[i], cudaStreamNonBlocking, lo);
+    cudaError_t e = cudaStreamCreateWithPriority(&s->pool[i], cudaStreamNonBlocking, i == 5 ? hi : lo);
     if (e != cudaSuccess) { pos_sched_destroy(s); return ctx_cuda_fail(c, e, "stream create"); }
   }
   if (cudaEventCreateWithFlags(&s->ev_end, cudaEventDisableTiming) != cudaSuccess) {

@@ -91,14 +91,27 @@ constexpr int TR = 4;               // tile-index ring depth (dynamic tile sched
 // computes a 256 x BN tile, each CTA holds its 128 rows of U and HALF of the tile's V columns,
 // so a stage is 2/3 the size and more stages fit — the large-K*P shapes are bound by operand
 // bytes in flight, not by W.
-template <bool kPair>
+// kWide (with kPair): the pair's tile is 256 x 2BN — two N = BN MMAs per k step into the two
+// halves of TMEM (one accumulator, no double buffering): 1/4 less operand bytes per output than
+// the 256 x BN tile, for the large-K*P shapes that are bound by L2 -> SM operand bytes.
+#ifndef POS_SFB_WSTAGES
+#define POS_SFB_WSTAGES 4
+#endif
+#ifndef POS_SFB_WWSLOTS
+#define POS_SFB_WWSLOTS 2
+#endif
+template <bool kPair, bool kWide = false>
 struct Lay {
-  static constexpr int kStages = kPair ? POS_SFB_PSTAGES : POS_SFB_STAGES;
-  static constexpr int kBCols = kPair ? BN / 2 : BN;          // V columns held per CTA
+  static_assert(!kWide || kPair, "the wide tile is a CTA-pair tile");
+  static constexpr int kStages = kWide ? POS_SFB_WSTAGES : (kPair ? POS_SFB_PSTAGES : POS_SFB_STAGES);
+  static constexpr int kBCols = (kPair && !kWide) ? BN / 2 : BN;   // V columns held per CTA
   static constexpr int kBBytes = KBYTES * kBCols;
   static constexpr int kStageBytes = A_BYTES + kBBytes;
-  static constexpr int kWSlots = kPair ? POS_SFB_PWSLOTS : POS_SFB_WSLOTS;   // W sub-tile ring depth
-  static constexpr int kEpi = kPair ? POS_SFB_PEPI : POS_SFB_EPI;             // epilogue warpgroups
+  static constexpr int kWSlots =                                   // W sub-tile ring depth
+      kWide ? POS_SFB_WWSLOTS : (kPair ? POS_SFB_PWSLOTS : POS_SFB_WSLOTS);
+  static constexpr int kEpi = kPair ? POS_SFB_PEPI : POS_SFB_EPI;   // epilogue warpgroups
+  static constexpr int kTN = kWide ? 2 * BN : BN;                   // tile columns
+  static constexpr int kAcc = kWide ? 1 : 2;                        // TMEM accumulators
   static constexpr int kThreads = 128 + 128 * kEpi;
   static constexpr int kData = kStages * kStageBytes + kWSlots * W_BYTES;
   static constexpr int kBars = 8 * (2 * kStages + 2 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
@@ -110,6 +123,7 @@ constexpr int TMEM_COLS = 2 * BN;
 
 static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 static_assert(Lay<true>::kTotal <= 232448, "shared memory budget (CTA pair)");
+static_assert(Lay<true, true>::kTotal <= 232448, "shared memory budget (wide CTA pair)");
 // A W slot must always be consumed by the same epilogue group: a group waits on a slot's full
 // barrier by phase parity, which is only sound if it consumed the slot's previous phase itself.
 static_assert(Lay<false>::kWSlots % Lay<false>::kEpi == 0 && Lay<true>::kWSlots % Lay<true>::kEpi == 0,
@@ -340,10 +354,11 @@ __host__ __device__ constexpr uint32_t instr_desc() {
          ((uint32_t)((kPair ? 2 * BM : BM) >> 4) << 24);
 }
 
-// number of W sub-tiles of the tile starting at column n0 that intersect [0, N)
+// number of W sub-tiles of a tile of TN columns starting at column n0 that intersect [0, N)
+template <int TN>
 __device__ __forceinline__ int nsub_of(int64_t N, int n0) {
   const int64_t s = (N - n0 + WSUB - 1) / WSUB;
-  return s < NSUB ? (int)s : NSUB;
+  return s < TN / WSUB ? (int)s : TN / WSUB;
 }
 
 struct TileInfo {
@@ -364,13 +379,17 @@ struct TileInfo {
 // need the same V columns, so each V box is loaded once and multicast to the two CTAs that hold it
 // — 1/4 less operand traffic through L2 than two independent pairs (the large-K*P shapes are bound
 // by L2 -> SM operand bytes).
-template <bool kTF32, bool kPair, bool kMc = false>
-__global__ void __launch_bounds__(Lay<kPair>::kThreads, 1)
+template <bool kTF32, bool kPair, bool kMc = false, bool kWide = false>
+__global__ void __launch_bounds__(Lay<kPair, kWide>::kThreads, 1)
 sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA2,
               const __grid_constant__ CUtensorMap tmB2, TileInfo ti, float alpha, int accumulate) {
-  using L = Lay<kPair>;
+  using L = Lay<kPair, kWide>;
+  static_assert(!(kMc && kWide), "one large-K*P variant at a time");
   constexpr int ST = L::kStages;             // operand ring depth
+  constexpr int TN = L::kTN, NACC = L::kAcc;
+  // V columns per CTA come in `kHalves` groups of kBH (wide pair: one group per MMA half)
+  constexpr int kHalves = kWide ? 2 : 1, kBH = L::kBCols / kHalves;
   constexpr int EB = kTF32 ? 4 : 2;          // element bytes
   constexpr int BK = KBYTES / EB;            // k rows per stage (64 bf16 / 32 tf32 at 128 B)
   constexpr int CHUNK = SWZ / EB;            // elements per 128-byte chunk along m / n
@@ -513,7 +532,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           }
         }
         const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM;
-        const int nb0 = (t % ti.nb_n) * BN + (int)prank * L::kBCols;   // this CTA's V columns
+        // this CTA's V columns: half h of the tile starts at n0 + h * BN; the pair splits each half
+        const int nb0 = (t % ti.nb_n) * TN + (int)prank * kBH;
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(b_empty + 8 * stage, phase ^ 1);
           const uint32_t sA = sbase + stage * L::kStageBytes, sB = sA + A_BYTES;
@@ -536,8 +556,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 tma_load_2d_pair_mc(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0, mask);
             } else {
 #pragma unroll
-              for (int c = 0; c < L::kBCols / CHUNK; ++c)
-                tma_load_2d_pair(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
+              for (int h = 0; h < kHalves; ++h)
+#pragma unroll
+                for (int c = 0; c < kBH / CHUNK; ++c)
+                  tma_load_2d_pair(mB, full, sB + (h * (kBH / CHUNK) + c) * BOX_BYTES,
+                                   nb0 + h * BN + c * CHUNK, k0);
             }
           } else {
             const uint32_t full = b_full + 8 * stage;
@@ -565,7 +588,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (t < 0) break;
         wait_ring(b_tempty + 8 * acc, aphase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * TN;
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(b_full + 8 * stage, phase);
           tc_fence_after();
@@ -573,15 +596,20 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk) {
             const uint64_t ad = smem_desc<kTF32>(sA + kk * UK * SWZ, BOX_BYTES);
-            const uint64_t bd = smem_desc<kTF32>(sB + kk * UK * SWZ, BOX_BYTES);
-            if (POS_SFB_EXP != 2 && POS_SFB_EXP != 3) umma<kTF32, kPair>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
+#pragma unroll
+            for (int h = 0; h < kHalves; ++h) {   // wide: the second N = BN half of the tile
+              const uint64_t bd =
+                  smem_desc<kTF32>(sB + h * (kBH / CHUNK) * BOX_BYTES + kk * UK * SWZ, BOX_BYTES);
+              if (POS_SFB_EXP != 2 && POS_SFB_EXP != 3)
+                umma<kTF32, kPair>(d_tmem + h * BN, ad, bd, IDESC, (kb | kk) != 0);
+            }
           }
           // frees the smem stage(s) when done (kMc: in all four CTAs — the V boxes are shared)
           umma_commit<kPair>(b_empty + 8 * stage, kMc ? 0xF : 0x3);
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         umma_commit<kPair>(b_tfull + 8 * acc, (uint16_t)(0x3u << pbase));   // accumulator ready
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
+        if (++acc == NACC) { acc = 0; aphase ^= 1; }
       }
     }
   } else if (warp == 2) {
@@ -592,8 +620,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int it = 0;; ++it) {
         const int t = tile_of(it, rphase);
         if (t < 0) break;
-        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
-        const int nsub = nsub_of(ti.N, n0);
+        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * TN;
+        const int nsub = nsub_of<TN>(ti.N, n0);
         for (int j = 0; j < nsub; ++j) {
           mbar_wait(b_wempty + 8 * ws, wphase ^ 1);
           const uint32_t wf = b_wfull + 8 * ws;
@@ -633,8 +661,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     for (int it = 0;; ++it) {
       const int t = tile_of(it, rphase);
       if (t < 0) break;
-      const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
-      const int nsub = nsub_of(ti.N, n0);
+      const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * TN;
+      const int nsub = nsub_of<TN>(ti.N, n0);
       // this group's sub-tiles of the tile: j = j0, j0 + EPI, ...; the last one frees TMEM
       const int j0 = (int)((g - (int)(sseq % EPI) + EPI) % EPI);
       const int jlast = j0 < nsub ? j0 + ((nsub - 1 - j0) / EPI) * EPI : -1;
@@ -642,11 +670,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tc_fence_after();
       // A4b fused: the gathered v rows carry a 1.0 in column N, so accumulator column N of the
       // tile holding it is sum_j U[j][m] — the bias gradient of row m
-      if (g == 0 && ti.bias && (int64_t)n0 <= ti.N && ti.N < (int64_t)n0 + BN) {
+      if (g == 0 && ti.bias && (int64_t)n0 <= ti.N && ti.N < (int64_t)n0 + TN) {
         uint32_t bv;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
                      : "=r"(bv)
-                     : "r"(tmem_base + lane_addr + acc * BN + (uint32_t)(ti.N - n0)));
+                     : "r"(tmem_base + lane_addr + acc * TN + (uint32_t)(ti.N - n0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int64_t m = (int64_t)m0 + et;
         if (m < ti.M) {
@@ -660,7 +688,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const int ws = (int)(s % WSLOTS);
         const uint32_t wphase = (s / WSLOTS) & 1;
         uint32_t r[32];
-        tmem_ld32(tmem_base + lane_addr + acc * BN + j * WSUB, r);
+        tmem_ld32(tmem_base + lane_addr + acc * TN + j * WSUB, r);
         if (j == jlast) release_acc(acc);     // accumulator fully drained by this thread
         mbar_wait(b_wfull + 8 * ws, wphase);
         if (POS_SFB_EXP == 1) {   // diagnostic: no W traffic (TMEM drained, slot recycled)
@@ -712,7 +740,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
       }
       sseq += (uint32_t)nsub;
-      if (++acc == 2) { acc = 0; aphase ^= 1; }
+      if (++acc == NACC) { acc = 0; aphase ^= 1; }
     }
     if (et == 0) bulk_wait_all();
   }
@@ -784,6 +812,21 @@ bool use_mc(int64_t KP) {
   return KP >= thr;
 }
 
+#ifndef POS_SFB_WIDE_KP
+#define POS_SFB_WIDE_KP (1LL << 40)   // off until measured (POS_SFB_WIDE=1 turns it on)
+#endif
+// wide pair tile (256 x 512, one TMEM accumulator) for K*P >= POS_SFB_WIDE_KP among the pair
+// shapes (env POS_SFB_WIDE=0|1 forces it off / on; POS_SFB_WIDE_KP overrides the threshold)
+bool use_wide(int64_t KP) {
+  if (const char* f = getenv("POS_SFB_WIDE")) {
+    if (f[0] == '0') return false;
+    if (f[0] == '1') return true;
+  }
+  int64_t thr = POS_SFB_WIDE_KP;
+  if (const char* e = getenv("POS_SFB_WIDE_KP")) thr = atoll(e);
+  return KP >= thr;
+}
+
 bool use_pair(int64_t KP) {
   if (const char* f = getenv("POS_SFB_PAIR")) {
     if (f[0] == '0') return false;
@@ -794,27 +837,27 @@ bool use_pair(int64_t KP) {
   return KP >= thr;
 }
 
-template <bool kTF32, bool kPair, bool kMc = false>
+template <bool kTF32, bool kPair, bool kMc = false, bool kWide = false>
 cudaError_t set_smem_attr() {
-  static cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32, kPair, kMc>,
+  static cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32, kPair, kMc, kWide>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              Lay<kPair>::kTotal);
+                                              Lay<kPair, kWide>::kTotal);
   return e;
 }
 
 // Co-resident clusters of the pair kernel (kMc: of the 4-CTA multicast kernel) on this device
 // (0 = cannot launch as clusters)
-template <bool kTF32, bool kMc>
+template <bool kTF32, bool kMc, bool kWide = false>
 int max_clusters() {
   static int n = -1;
   constexpr unsigned kCl = kMc ? 4 : 2;
   if (n < 0) {
     n = 0;
-    if (set_smem_attr<kTF32, true, kMc>() == cudaSuccess) {
+    if (set_smem_attr<kTF32, true, kMc, kWide>() == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(kCl * (unsigned)num_sms());
-      cfg.blockDim = dim3(Lay<true>::kThreads);
-      cfg.dynamicSmemBytes = Lay<true>::kTotal;
+      cfg.blockDim = dim3(Lay<true, kWide>::kThreads);
+      cfg.dynamicSmemBytes = Lay<true, kWide>::kTotal;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = kCl;
@@ -823,14 +866,15 @@ int max_clusters() {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int c = 0;
-      if (cudaOccupancyMaxActiveClusters(&c, sfb_tc_kernel<kTF32, true, kMc>, &cfg) == cudaSuccess)
+      if (cudaOccupancyMaxActiveClusters(&c, sfb_tc_kernel<kTF32, true, kMc, kWide>, &cfg) ==
+          cudaSuccess)
         n = c;
       else
         clear_stale_launch_error();
     }
     if (getenv("POS_SFB_VERBOSE"))
       fprintf(stderr, "[poseidon] sfb_tc %s kernel: %d co-resident clusters of %u (%d SMs)\n",
-              kMc ? "multicast" : "pair", n, kCl, num_sms());
+              kMc ? "multicast" : (kWide ? "wide pair" : "pair"), n, kCl, num_sms());
   }
   return n;
 }
@@ -870,7 +914,7 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
     pl->tmB2 = pl->tmB;
   }
   pl->M = M; pl->N = N; pl->KP = KP;
-  pl->nb_n = (int)((NB + BN - 1) / BN);
+  int64_t TN = BN;   // tile columns (the wide pair tile: 2 BN), set once the variant is chosen
   pl->bias = bias;
   pl->nkb = (int)((KP + BK - 1) / BK);
   pl->tf32 = kTF32;
@@ -878,6 +922,9 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
   pl->pair = use_pair(KP) && ctas >= 2 && max_pairs<kTF32>() > 0;
   pl->mc = pl->pair && use_mc(KP) && ctas >= 4 && max_clusters<kTF32, true>() > 0;
+  pl->wide = pl->pair && !pl->mc && use_wide(KP) && max_clusters<kTF32, false, true>() > 0;
+  if (pl->wide) TN = 2 * BN;
+  pl->nb_n = (int)((NB + TN - 1) / TN);
   const int cl = pl->mc ? 4 : (pl->pair ? 2 : 1);   // CTAs per scheduling unit
   const int64_t rows = (int64_t)cl * BM;
   const int64_t tiles = (int64_t)pl->nb_n * ((M + rows - 1) / rows);
@@ -887,17 +934,18 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
   // usable SM cannot host a pair; a cluster that waits for a second wave would be a straggler)
   int units = ctas;
   if (pl->mc) units = std::min(ctas / 4, max_clusters<kTF32, true>());
+  else if (pl->wide) units = std::min(ctas / 2, max_clusters<kTF32, false, true>());
   else if (pl->pair) units = std::min(ctas / 2, max_pairs<kTF32>());
   if (units > pl->num_tiles) units = pl->num_tiles;
   pl->grid = cl * units;
   return true;
 }
 
-template <bool kTF32, bool kPair, bool kMc = false>
+template <bool kTF32, bool kPair, bool kMc = false, bool kWide = false>
 cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
   clear_stale_launch_error();
-  constexpr int smem_bytes = Lay<kPair>::kTotal;
-  if (cudaError_t e = set_smem_attr<kTF32, kPair, kMc>(); e != cudaSuccess) return e;
+  constexpr int smem_bytes = Lay<kPair, kWide>::kTotal;
+  if (cudaError_t e = set_smem_attr<kTF32, kPair, kMc, kWide>(); e != cudaSuccess) return e;
   TileInfo ti;
   ti.M = pl.M; ti.N = pl.N; ti.KP = pl.KP;
   ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
@@ -910,7 +958,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   if constexpr (kPair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.grid);
-    cfg.blockDim = dim3(Lay<true>::kThreads);
+    cfg.blockDim = dim3(Lay<true, kWide>::kThreads);
     cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -920,8 +968,8 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true, kMc>, pl.tmA, pl.tmB, pl.tmW,
-                              pl.tmA2, pl.tmB2, ti, alpha, accumulate);
+    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true, kMc, kWide>, pl.tmA, pl.tmB,
+                              pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
   } else {
     sfb_tc_kernel<kTF32, false><<<pl.grid, Lay<false>::kThreads, smem_bytes, s>>>(
         pl.tmA, pl.tmB, pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
@@ -954,6 +1002,9 @@ cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cuda
   if (pl.mc)
     return pl.tf32 ? launch_plan_impl<true, true, true>(pl, alpha, accumulate, s)
                    : launch_plan_impl<false, true, true>(pl, alpha, accumulate, s);
+  if (pl.wide)
+    return pl.tf32 ? launch_plan_impl<true, true, false, true>(pl, alpha, accumulate, s)
+                   : launch_plan_impl<false, true, false, true>(pl, alpha, accumulate, s);
   if (pl.pair)
     return pl.tf32 ? launch_plan_impl<true, true>(pl, alpha, accumulate, s)
                    : launch_plan_impl<false, true>(pl, alpha, accumulate, s);

@@ -228,7 +228,10 @@ __device__ __forceinline__ void ps_st1(const PsArgs& a, int64_t j, float v) {
 }
 
 template <bool kRedMc, bool kStMc>
-__global__ void __launch_bounds__(kPsThreads) ps_sync_kernel(PsArgs a, Xg x) {
+// minBlocks 2 caps the registers at 64 per thread, so a PS CTA (512 threads, 32K registers) fits on an
+// SM next to a resident reconstruction CTA (256 threads x 120 registers): the fused PS units run
+// concurrently with the reconstructions instead of waiting for their SMs to drain
+__global__ void __launch_bounds__(kPsThreads, 2) ps_sync_kernel(PsArgs a, Xg x) {
   ktrace_begin(a.trace);
   ktrace_begin(a.group);
   if (!xg_enter(x)) return;
