@@ -104,7 +104,11 @@ struct pos_sched {
   int last_sfb = -1;       // most recently issued SFB unit of this iteration
   bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
   int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1: one, in order)
-  bool pack_stream = true;    // flag-mode packs on their own stream (POS_PACK_STREAM=0: comm stream)
+  // flag-mode packs on their own stream (POS_PACK_STREAM=1) instead of the comm stream: the PS
+  // chain then starts with the first dense unit. Measured at P = 2 (round 2): VGG19 -7%, IncV3
+  // -4%, but VGG19-22K +7% and AlexNet +17% (the packs gate the reconstructions there and slow
+  // down next to the PS kernels) — off by default
+  bool pack_stream = false;
   int n_sfb = 0;              // SFB units registered
   bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
   // POS_SCHED_TRACE: one group record per scheme (all of a step's PS / SFB apply kernels)
@@ -425,7 +429,7 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   s->flags = flags;
   s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
   if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = atoi(e) > 1 ? 2 : 1;
-  if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] != '0';
+  if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] == '1';
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
   int lo = 0, hi = 0;

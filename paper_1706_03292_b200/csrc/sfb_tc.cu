@@ -23,9 +23,14 @@
 //
 //  * K*P >= 1024: CTA-pair variant (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA
 //    stages its 128 rows of U and half of the tile's V columns, the even CTA issues the MMAs
-//    for both; 1/3 less operand traffic and smaller stages (more in flight) where the operand
-//    stream, not W, is the bound. Measured (profiles/r01/README.md): +10% at K*P = 1024, +2% at 512,
-//    -2% at K*P <= 256 (the single-CTA kernel stays there).
+//    for both; 1/3 less operand traffic and smaller stages (5 x 32 KB in flight + 4 W slots)
+//    where the operand stream, not W, is the bound. At K*P = 1024 the kernel is bound by the
+//    bytes each SM can keep in flight from L2 (operands 16 B + W 4 B per output element; the
+//    diagnostic builds POS_SFB_EXP show MMA+operands alone at 0.95 of the tensor peak and the W
+//    path alone at 0.92 of HBM — DESIGN.md §10). Rejected variants kept as compile-time options:
+//    4-CTA clusters with TMA multicast of V (POS_SFB_MC; only 33 clusters of 4 co-reside = 132
+//    SMs), a 256 x 512 pair tile with one TMEM accumulator (POS_SFB_WIDE; loses the epilogue /
+//    MMA overlap), a dedicated W storer thread (POS_SFB_STORER).
 //
 // Warp roles (256 threads): w0 operand TMA producer, w1 MMA issuer + TMEM owner, w2 W TMA
 // producer, w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes 32*(w%4) .. +31 = tile rows).
@@ -56,7 +61,7 @@ constexpr int BN = POS_SFB_BN;      // tile cols (n) = UMMA N = TMEM columns per
 #define POS_SFB_WSLOTS 5
 #endif
 #ifndef POS_SFB_PWSLOTS
-#define POS_SFB_PWSLOTS 5
+#define POS_SFB_PWSLOTS 4
 #endif
 // The kernel is bound by the W read-modify-write (8 B per element): shared memory goes to W
 // prefetch depth (WSLOTS x 16 KB in flight per SM) rather than to operand stages (K*P is small).
@@ -72,7 +77,13 @@ constexpr int A_BYTES = KBYTES * BM;     // per stage: BK rows x BM elements (an
 constexpr int W_BYTES = BM * WSUB * 4;
 constexpr int TR = 4;               // tile-index ring depth (dynamic tile scheduler)
 #ifndef POS_SFB_PSTAGES
-#define POS_SFB_PSTAGES 4
+#define POS_SFB_PSTAGES 5   // round 2: 5 stages + 4 W slots beat 4 + 5 at K*P >= 1024 (83 -> 79.5 us, AlexNet fc6)
+#endif
+// W store issue: 0 = epilogue thread 0 issues the TMA store of a sub-tile and retires the slot one
+// sub-tile later; 1 = a dedicated storer thread (warp 3) issues the stores and frees each slot as
+// soon as its store has read shared memory (the epilogue never waits on a store)
+#ifndef POS_SFB_STORER
+#define POS_SFB_STORER 0
 #endif
 // Diagnostics only (never in the shipped build): 1 = no W traffic in the epilogue, 2 = no MMAs,
 // 3 = no MMAs and no operand loads.
@@ -114,7 +125,7 @@ struct Lay {
   static constexpr int kAcc = kWide ? 1 : 2;                        // TMEM accumulators
   static constexpr int kThreads = 128 + 128 * kEpi;
   static constexpr int kData = kStages * kStageBytes + kWSlots * W_BYTES;
-  static constexpr int kBars = 8 * (2 * kStages + 2 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
+  static constexpr int kBars = 8 * (2 * kStages + 3 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
   static constexpr int kTotal = kData + kBars + 1024;         // + alignment slack
 };
 constexpr int STAGE_BYTES = Lay<false>::kStageBytes;
@@ -404,7 +415,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   constexpr int kDrainers = 4 * EPI * (kPair ? 2 : 1);
   // tile-ring consumers: (MMA issuer | peer operand producer) + W producer + epilogue, per CTA
   // (kMc: the second pair's leader is both an MMA issuer and a ring-reading operand producer)
-  constexpr int kRingConsumers = (2 + 128 * EPI) * kCl + (kMc ? 1 : 0);
+  constexpr int kRingConsumers = (2 + 128 * EPI + (POS_SFB_STORER ? 1 : 0)) * kCl + (kMc ? 1 : 0);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -416,7 +427,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const uint32_t b_wfull = b_empty + 8 * ST, b_wempty = b_wfull + 8 * WSLOTS;
   const uint32_t b_tfull = b_wempty + 8 * WSLOTS, b_tempty = b_tfull + 16;
   const uint32_t b_rfull = b_tempty + 16, b_rempty = b_rfull + 8 * TR;   // tile-index ring
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 2 * WSLOTS + 4 + 2 * TR);
+  const uint32_t b_wupd = b_rempty + 8 * TR;   // W slot updated by the epilogue (storer mode)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 3 * WSLOTS + 4 + 2 * TR);
   volatile int* tile_ring = reinterpret_cast<volatile int*>(tmem_slot + 4);
   const bool dyn = ti.counter != nullptr;
   // CTA pair: the even CTA (rank 0) fetches tiles, issues the MMAs and owns the shared
@@ -453,7 +465,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   if (threadIdx.x == 0) {
     // kMc: a stage is free only when BOTH pairs' MMAs have read it (its V boxes were multicast)
     for (int i = 0; i < ST; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, kMc ? 2 : 1); }
-    for (int i = 0; i < WSLOTS; ++i) { mbar_init(b_wfull + 8 * i, 1); mbar_init(b_wempty + 8 * i, 1); }
+    for (int i = 0; i < WSLOTS; ++i) {
+      mbar_init(b_wfull + 8 * i, 1);
+      mbar_init(b_wempty + 8 * i, 1);
+      mbar_init(b_wupd + 8 * i, 1);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(b_tfull + 8 * i, 1);
       mbar_init(b_tempty + 8 * i, kDrainers);
@@ -638,6 +654,29 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
       }
     }
+  } else if (warp == 3) {
+    // ===================== W sub-tile storer (POS_SFB_STORER) =====================
+    if (POS_SFB_STORER && lane == 0) {
+      int ws = 0;
+      uint32_t uphase = 0, rphase = 0;
+      for (int it = 0;; ++it) {
+        const int t = tile_of(it, rphase);
+        if (t < 0) break;
+        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * TN;
+        const int nsub = nsub_of<TN>(ti.N, n0);
+        for (int j = 0; j < nsub; ++j) {
+          mbar_wait(b_wupd + 8 * ws, uphase);       // the epilogue has updated the slot
+          if (POS_SFB_EXP != 1) {
+            tma_store_2d(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
+            bulk_commit();
+            bulk_wait_read<0>();                     // the store has read the slot
+          }
+          mbar_arrive(b_wempty + 8 * ws);            // the W producer may refill it
+          if (++ws == WSLOTS) { ws = 0; uphase ^= 1; }
+        }
+      }
+      bulk_wait_all();
+    }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> regs, W += alpha * acc in smem, TMA store ========
     const int g = (warp - 4) >> 2;            // epilogue warpgroup
@@ -693,7 +732,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         mbar_wait(b_wfull + 8 * ws, wphase);
         if (POS_SFB_EXP == 1) {   // diagnostic: no W traffic (TMEM drained, slot recycled)
           named_bar_sync(1 + g, 128);
-          if (et == 0) mbar_arrive(b_wempty + 8 * ws);
+          if (et == 0) mbar_arrive((POS_SFB_STORER ? b_wupd : b_wempty) + 8 * ws);
           continue;
         }
         const uint32_t row = sW0 + ws * W_BYTES + et * SWZ;
@@ -721,7 +760,9 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         fence_proxy_async_smem();             // generic-proxy smem writes -> visible to TMA
         named_bar_sync(1 + g, 128);
-        if (et == 0) {
+        if (POS_SFB_STORER) {
+          if (et == 0) mbar_arrive(b_wupd + 8 * ws);   // the storer thread takes it from here
+        } else if (et == 0) {
           if (POS_SFB_L2HINT)
             tma_store_2d_hint(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0, policy_evict_first());
           else
@@ -742,7 +783,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       sseq += (uint32_t)nsub;
       if (++acc == NACC) { acc = 0; aphase ^= 1; }
     }
-    if (et == 0) bulk_wait_all();
+    if (!POS_SFB_STORER && et == 0) bulk_wait_all();
   }
 
   tc_fence_before();
