@@ -477,11 +477,19 @@ def run_ours(a):
             if bb["kind"] == "dense":
                 bb["g"].copy_(bb["g0"])
 
+    def check_async(where):
+        # a cross-GPU wait that exceeded the watchdog (POS_TIMEOUT_MS) or an asynchronous CUDA
+        # error: fail loudly instead of timing steps whose waits each run into the timeout
+        rc = ctx.async_error()
+        if rc < 0:
+            raise pos.PoseidonError(rc, f"bench ({where}, rank {rank})")
+
     # ---- warmup (untimed, eager: NCCL connections, launch plans) ----
     _log(f"{len(units)} units registered; warmup")
     for _ in range(a.warmup):
         step(main)
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        check_async("warmup")
     _log("warmup done")
     graphs = g_e2e = run_e2e = None
     if a.eager:
@@ -493,6 +501,7 @@ def run_ours(a):
         for i in range(len(graphs)):
             run(i)
     torch.cuda.synchronize()
+    check_async("graph warmup")
     _log("graph warmup done")
     refresh_grads()      # reduce-scatter sums in place; start the timed region from fresh gradients
     torch.cuda.synchronize()
@@ -518,6 +527,7 @@ def run_ours(a):
     ms = evs[0].elapsed_time(evs[-1]) / a.steps
     per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(a.steps)]
     _log(f"timed region done: {ms:.4f} ms/step")
+    check_async("timed region")
     if world > 1:
         t = torch.tensor([ms] + per_step, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)          # max over ranks (per step)

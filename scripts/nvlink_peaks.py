@@ -82,13 +82,14 @@ if rank == 0:
     res[f"P{world}"] = {
         "ag_busbw_gbs": max(r["ag_busbw_gbs"] for r in rows),
         "rs_busbw_gbs": max(r["rs_busbw_gbs"] for r in rows),
-        "per_dir_gbs": max(max(r["ag_busbw_gbs"], r["rs_busbw_gbs"]) for r in rows),
+        # the best per-direction rate any method reached: NCCL AG / RS or the fused PS unit
+        "per_dir_gbs": max(max(r["ag_busbw_gbs"], r["rs_busbw_gbs"], r.get("ps_nvls_busbw_gbs", 0)) for r in rows),
         "ps_nvls_busbw_gbs": max(r.get("ps_nvls_busbw_gbs", 0) for r in rows),
         "ps_rank_order_busbw_gbs": max(r.get("ps_rank_order_busbw_gbs", 0) for r in rows),
         "sizes": rows,
         "how": "nccl-tests style in-place AG / RS fp32 (torch.distributed, NCCL " +
                ".".join(map(str, torch.cuda.nccl.version())) + "), device time max over ranks, "
-               "median of 3 x 20 launches; busbw = algbw (P-1)/P",
+               "median of 3 x 20 launches; busbw = algbw (P-1)/P; per_dir_gbs = max(NCCL AG, NCCL RS, the fused PS unit's RS+AG-equivalent busbw)",
         "gpu": torch.cuda.get_device_name(dev),
     }
     os.makedirs(os.path.dirname(out_path), exist_ok=True)
