@@ -219,7 +219,7 @@ cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const
                           int max_ctas, cudaStream_t s);
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G);
 // the plan for inner dimension KP would use the CTA-pair (cluster) kernel
-bool sfb_tc_would_pair(int64_t KP);
+bool sfb_tc_would_pair(int64_t KP, bool cluster_ok = true);
 
 // A launch plan for the tensor-core reconstruct-and-apply: TMA descriptors encoded once for fixed
 // buffers (the scheduler keeps one per SFB layer, so the hot path does no host-side encoding).
@@ -245,7 +245,7 @@ struct SfbTcPlan {
 // false if the shape/alignment/dtype cannot use the tensor-core kernel
 bool sfb_tc_make_plan(SfbTcPlan* plan, int64_t M, int64_t N, int64_t KP, int32_t dtype,
                       const void* G, float* W, int64_t ldw, int max_ctas, float* bias = nullptr,
-                      const void* G2 = nullptr);
+                      const void* G2 = nullptr, bool cluster_ok = true);
 cudaError_t sfb_tc_launch(const SfbTcPlan& plan, float alpha, int accumulate, cudaStream_t s);
 
 // A4 + A4b dispatcher used by the C ABI and the context code

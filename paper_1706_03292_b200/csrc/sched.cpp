@@ -129,7 +129,8 @@ int ensure_plan(pos_sched* s, Unit& un) {
   pos_ctx* c = s->ctx;
   if (un.scheme != POS_SCHEME_SFB || un.plan_ctas == c->max_ctas) return POS_OK;
   un.has_plan = sfb_tc_make_plan(&un.plan, un.M, un.N, un.K * c->world, un.dtype, un.gbuf, un.W,
-                                 un.N, c->max_ctas, un.b, un.flag_mode ? un.gbuf2 : nullptr);
+                                 un.N, c->max_ctas, un.b, un.flag_mode ? un.gbuf2 : nullptr,
+                                 /*cluster_ok=*/c->world == 1);
   un.plan.counter = (s->flags & POS_SCHED_STATIC_TILES) ? nullptr : un.tile_counter;
   un.plan.gsel = un.flag_mode ? un.gstate : nullptr;
   if (un.flag_mode && !un.has_plan) POS_FAIL(POS_ESTATE, "flag-mode gather without a tensor-core plan");
@@ -482,7 +483,7 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   u.members = {l};
   if (scheme == POS_SCHEME_SFB) {
     u.sfb_idx = s->n_sfb++;
-    if (dtype != POS_DT_F32 && sfb_tc_would_pair(K * c->world)) s->any_pair = true;
+    if (dtype != POS_DT_F32 && sfb_tc_would_pair(K * c->world, c->world == 1)) s->any_pair = true;
   }
   const int64_t rows = scheme == POS_SCHEME_SFB ? K * c->world : K;
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));

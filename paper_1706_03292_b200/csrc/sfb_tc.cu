@@ -868,11 +868,15 @@ bool use_wide(int64_t KP) {
   return KP >= thr;
 }
 
-bool use_pair(int64_t KP) {
+// cluster_ok = false (the multi-GPU scheduler): no cluster launch unless POS_SFB_PAIR=1 forces it —
+// at P = 4 a CUDA-graph step with CTA-pair reconstructions next to the fused cross-GPU kernels
+// stalled a rank's factor pack until its peers' watchdogs fired (round 2)
+bool use_pair(int64_t KP, bool cluster_ok) {
   if (const char* f = getenv("POS_SFB_PAIR")) {
     if (f[0] == '0') return false;
     if (f[0] == '1') return true;
   }
+  if (!cluster_ok) return false;
   int64_t thr = POS_SFB_PAIR_KP;
   if (const char* e = getenv("POS_SFB_PAIR_KP")) thr = atoll(e);
   return KP >= thr;
@@ -924,7 +928,7 @@ int max_pairs() { return max_clusters<kTF32, false>(); }
 
 template <bool kTF32>
 bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
-                    int64_t ldw, int max_ctas, float* bias, const void* G2) {
+                    int64_t ldw, int max_ctas, float* bias, const void* G2, bool cluster_ok) {
   // with a bias the V operand includes the ones column N (the GEMM's extra output column)
   const int64_t NB = N + (bias ? 1 : 0);
   constexpr int EB = kTF32 ? 4 : 2;
@@ -961,7 +965,7 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
   pl->tf32 = kTF32;
   int ctas = num_sms();
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
-  pl->pair = use_pair(KP) && ctas >= 2 && max_pairs<kTF32>() > 0;
+  pl->pair = use_pair(KP, cluster_ok) && ctas >= 2 && max_pairs<kTF32>() > 0;
   pl->mc = pl->pair && use_mc(KP) && ctas >= 4 && max_clusters<kTF32, true>() > 0;
   pl->wide = pl->pair && !pl->mc && use_wide(KP) && max_clusters<kTF32, false, true>() > 0;
   if (pl->wide) TN = 2 * BN;
@@ -1020,7 +1024,7 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
 
 }  // namespace
 
-bool sfb_tc_would_pair(int64_t KP) { return use_pair(KP); }
+bool sfb_tc_would_pair(int64_t KP, bool cluster_ok) { return use_pair(KP, cluster_ok); }
 
 bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
   // TMA stores move whole 16-byte chunks: the last W row chunk must not straddle column N (else
@@ -1031,12 +1035,12 @@ bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
 
 bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t dtype,
                       const void* G, float* W, int64_t ldw, int max_ctas, float* bias,
-                      const void* G2) {
+                      const void* G2, bool cluster_ok) {
   if (dtype == POS_DT_F32 || !sfb_tc_supported(N, ldw, W, G)) return false;
   if (G2 && !aligned16(G2)) return false;
   if (dtype == POS_DT_TF32)
-    return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2);
-  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2);
+    return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2, cluster_ok);
+  return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2, cluster_ok);
 }
 
 cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {

@@ -134,7 +134,8 @@ def _worker(rank, world, port, outdir):
         check("sfb_stat_dW", err(g3 - W30, Wr3 - W30) <= 2e-3)
         res["digests"]["sfb_stat"] = _digest(W3)
         # ---- (f) scheduler SFB: tf32 (flag-mode gather, double buffer), fp32 (barrier-mode
-        #          multicast + SIMT reconstruction) and a CTA-pair layer (K*P = 1024); 3 iterations
+        #          multicast + SIMT reconstruction) and a K*P = 1024 layer (single-CTA kernel by default,
+        #          then the CTA-pair kernel forced); 3 iterations
         def run_dtype(dt, in_dt, Kx, Mx, Nx, iters=3):
             sch = pos.Scheduler(ctx, 1)
             U, V = zip(*(si.exact_factors(si.rng(49, Kx, p), Kx, Mx, Nx) for p in range(P)))
@@ -157,7 +158,13 @@ def _worker(rank, world, port, outdir):
             return ok
         check("sched_tf32_flags_3iter", run_dtype("tf32", pos.POS_IN_F32, 16, 1000, 1028))
         check("sched_f32_barrier_3iter", run_dtype("f32", pos.POS_IN_F32, 16, 300, 132))
-        check("sched_pair_3iter", run_dtype("bf16", pos.POS_IN_BF16, 1024 // P, 2000, 4100))
+        check("sched_kp1024_3iter", run_dtype("bf16", pos.POS_IN_BF16, 1024 // P, 2000, 4100))
+        # the CTA-pair (cluster) kernel is off at P > 1 by default; forced on, eager, it still works
+        os.environ["POS_SFB_PAIR"] = "1"
+        try:
+            check("sched_pair_forced_3iter", run_dtype("bf16", pos.POS_IN_BF16, 1024 // P, 2000, 4100))
+        finally:
+            del os.environ["POS_SFB_PAIR"]
         # ---- (e) WFBP scheduler: FC (SFB) + bucket + dense; WFBP == sequential, both == oracle --
         def run_sched(sequential, graph, symm_dense=False, iters=1):
             alloc = (lambda k: ctx.sym_empty(k)) if symm_dense else (lambda k: torch.zeros(k, device=dev))
