@@ -89,7 +89,11 @@ class Wfbp:
     which is the forward order of sequential CNNs; backward triggers arrive in reverse).
 
     force_ps: names (as in model.named_modules()) of nn.Linear layers to synchronise by PS instead
-    of Algorithm 1's choice. per_layer_gate: gate each layer's next forward on its own sync."""
+    of Algorithm 1's choice. per_layer_gate: gate each layer's next forward on its own sync.
+
+    Construct it on the stream that will run the training steps (for CUDA-graph capture: the
+    capture stream): the post-accumulate-grad hooks keep every dense parameter's AccumulateGrad node
+    alive, and autograd synchronises each backward with the stream that node was created on."""
 
     def __init__(self, model: nn.Module, ctx: Context, batch_per_gpu: int, bucket_mb: float = 16.0,
                  dtype: str = "bf16", factor_dtype=torch.bfloat16, sequential: bool = False,

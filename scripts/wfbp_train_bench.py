@@ -76,7 +76,16 @@ def main():
     g = torch.Generator(device=dev)
     g.manual_seed(rank)
 
+    # every arm is built, warmed up and captured on ONE side stream: the post-accumulate-grad hooks
+    # keep each parameter's AccumulateGrad node alive, and torch syncs a backward with the stream the
+    # node was created on — the legacy default stream would break graph capture
+    side = torch.cuda.Stream()
+
     def run(mode):
+        with torch.cuda.stream(side):
+            return _run(mode)
+
+    def _run(mode):
         model, res, ncls = build_model(model_name, dev)
         wf = opt = None
         if mode == "local":
@@ -117,15 +126,11 @@ def main():
         torch.cuda.synchronize()
         run_step = step
         if a.graph:
-            side = torch.cuda.Stream()
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                for _ in range(3):
-                    step()
-            torch.cuda.current_stream().wait_stream(side)
+            for _ in range(3):
+                step()
             torch.cuda.synchronize()
             gph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gph):
+            with torch.cuda.graph(gph, stream=side):
                 g_loss = step()
             torch.cuda.synchronize()
 
