@@ -173,6 +173,8 @@ static int ctx_common_init(pos_ctx* c) {
   *h = 0;
   c->err_host = h;
   POS_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), h, 0));
+  // POS_REDUCE_ORDER=1: fixed rank-order reduce in the fused PS kernel (pos_set_reduce_order)
+  if (env_int("POS_REDUCE_ORDER", 0) == 1) c->reduce_order = POS_REDUCE_RANK_ORDER;
   const int64_t ms = env_int("POS_TIMEOUT_MS", 20000);
   c->timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
   return POS_OK;

@@ -608,12 +608,14 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   const Xg x = make_xg(c, kSitePsEntry);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
   const int grid = ps_grid(c, n, P);
-  // P = 2 option (POS_PS_P2P=1): plain peer loads / stores move less over NVLink than the switch
-  // path — faster alone, but its NVLink traffic through the SMs' load/store path slows a
-  // concurrent reconstruction more (round-1 measurement); the NVLS kernel stays the default
+  // P = 2: plain peer loads (summed in rank order: deterministic) + unicast peer stores move n/2 +
+  // n/2 words per GPU and direction where the switch path moves ~1.5 n. Round 1 kept NVLS (the peer
+  // path slowed a co-running reconstruction more); with the PS CTAs now co-resident with the
+  // reconstruction and 64 MiB buckets, the peer path wins at P = 2 (round 2: VGG19-22K 0.426 ->
+  // 0.338 ms, Inception-V3 0.296 -> 0.282 ms). POS_PS_P2P=0 selects the NVLS kernel.
   static const bool p2p2 = [] {
     const char* e = getenv("POS_PS_P2P");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   cudaError_t e = cudaSuccess;
   if (c->fault == POS_FAULT_SKIP_PS && c->fault_rank == c->rank) {

@@ -1,7 +1,7 @@
 """North-star full-model parity (north_star "VGG19-22K full-model synchronisation
 ... that matches the oracle"; "229M parameters", "91% ... FC").
 
-This runs bench.py's OWN step — bench.plan_units (16 MiB dense buckets), bench.register_units,
+This runs bench.py's OWN step — bench.plan_units (bench.DEFAULT_BUCKET_MB dense buckets), bench.register_units,
 bench.make_step (every layer triggered in backward order through the WFBP scheduler) and
 bench.capture_ring (the 4-graph CUDA-graph ring bench.py replays), in bench.py's order: eager
 warm-up steps, then graph replays — on host-generated inputs, and compares EVERY layer's W (and
@@ -63,7 +63,8 @@ class HostFill:
         return si.exact_dense_grad(g, n) if self.regime == "exact" else si.stat_dense_grad(g, n)
 
 
-def run_model(config, regime, sequential=False, graphs=True, bucket_mb=16.0):
+def run_model(config, regime, sequential=False, graphs=True, bucket_mb=None):
+    bucket_mb = bench.DEFAULT_BUCKET_MB if bucket_mb is None else bucket_mb
     model_name, K = si.CONFIGS[config]
     model = si.load_model(model_name)
     ctx = pos.Context.from_unique_id(bytes(128), 1, 0)
@@ -115,8 +116,9 @@ def oracle_model(model, host, n_iter, alpha, others=()):
     return ref
 
 
-def test_vgg19_22k_bench_step_graph_ring_exact_bitwise():
-    model, host, got, n_iter, alpha = run_model("c3", "exact")
+@pytest.mark.parametrize("bucket_mb", [None, 16.0, 0.0])   # bench default; 16 MiB; one unit per layer
+def test_vgg19_22k_bench_step_graph_ring_exact_bitwise(bucket_mb):
+    model, host, got, n_iter, alpha = run_model("c3", "exact", bucket_mb=bucket_mb)
     assert model.total_params == 229052817 and len(model.layers) == 19
     ref = oracle_model(model, host, n_iter, alpha)
     for l, ly in enumerate(model.layers):
