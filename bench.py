@@ -39,7 +39,17 @@ import synth_inputs as si  # noqa: E402
 
 METRIC = "grad_sync_params_per_s"
 UNIT = "params/s"
-DEFAULT_BUCKET_MB = 64.0   # PS unit size of the timed plan (--bucket-mb)
+
+
+def default_bucket_mb(P):
+    """PS unit size of the timed plan (--bucket-mb default). Each fused cross-GPU PS unit costs
+    ~17 us of fixed latency, so fewer, larger units win while the PS chain is exposed: measured on
+    VGG19-22K, 64 MiB at P <= 2 (P = 2: 0.338 vs 0.375 ms with 16 MiB), 16 MiB at P >= 4 (P = 4:
+    0.366 vs 0.412 ms with 64 MiB — there the big unit, issued last, ends the step)."""
+    return 64.0 if P <= 2 else 16.0
+
+
+DEFAULT_BUCKET_MB = default_bucket_mb(1)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_GBS_PER_DIR = 770.0   # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
@@ -82,11 +92,10 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "tf32", "f32"])
     ap.add_argument("--sequential", action="store_true", help="WFBP off: sync after the whole step")
     ap.add_argument("--max-ctas", type=int, default=0)
-    ap.add_argument("--bucket-mb", type=float, default=DEFAULT_BUCKET_MB,
+    ap.add_argument("--bucket-mb", type=float, default=None,
                     help="PS unit = consecutive dense layers up to this many MiB of fp32 (the paper "
-                         "moves PS traffic in 2 MB KV pairs; each fused cross-GPU unit costs ~17 us "
-                         "of fixed latency on B200, so 64 MiB measured best at P = 2); 0 = one unit "
-                         "per layer")
+                         "moves PS traffic in 2 MB KV pairs); default default_bucket_mb(P): 64 at "
+                         "P <= 2, 16 at P >= 4; 0 = one unit per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tf32", action="store_true", help="skip the extra tf32-factor measurement")
@@ -467,6 +476,8 @@ def run_ours(a):
 
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * 1 + rank)
+    if a.bucket_mb is None:
+        a.bucket_mb = default_bucket_mb(P)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
     # The timed region replays UNTRACED step graphs. In-step kernel times come from a second ring
     # of the same step captured with device-side tracing (the kernels stamp %globaltimer; no timing

@@ -120,7 +120,7 @@ def _bench_worker(rank, world):
     import bench
     import synth_inputs as si
     model = si.load_model("vgg19_22k")
-    units = bench.plan_units(model, int(bench.DEFAULT_BUCKET_MB * 2 ** 20 / 4))
+    units = bench.plan_units(model, int(bench.default_bucket_mb(world) * 2 ** 20 / 4))
     rows = bench.unit_accounting(model, units, 32, world, "bf16")
     blob = repr([(r["name"], r["params"], r["hbm_a4"], r["nvl"]) for r in rows]).encode()
     t = torch.tensor(list(blob[:4096]) + [0] * (4096 - len(blob[:4096])), dtype=torch.int64)

@@ -69,7 +69,7 @@ def _worker(rank, world, port, outdir):
         # ---- (a) full VGG19-22K, bench step, graph ring, exact regime ----------------------------
         model_name, K = si.CONFIGS["c3"]
         model = si.load_model(model_name)
-        units = bench.plan_units(model, int(bench.DEFAULT_BUCKET_MB * 2 ** 20 / 4))
+        units = bench.plan_units(model, int(bench.default_bucket_mb(P) * 2 ** 20 / 4))
         sch = pos.Scheduler(ctx, len(model.layers), timing="apply")
         fill = HostFill("exact", K, rank=rank)
         bufs = bench.register_units(pos, ctx, sch, model, units, K, "bf16", fill)
