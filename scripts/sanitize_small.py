@@ -57,5 +57,49 @@ ok &= np.array_equal(Wd.cpu().numpy().astype(np.float64), W2) and np.array_equal
 ok &= np.array_equal(Wn[:nd].cpu().numpy().astype(np.float64), sync.ps_update(sync.ps_update(wn, [gn], si.EXACT_ALPHA), [gn], si.EXACT_ALPHA))
 sch.timing(1)
 sch.close(); c1.close(); ctx.close()
+# loopback: the P > 1 kernel bodies (flag-mode pack + multicast-slot stores through the pointer
+# table, ready flags, flag wait, double-buffered reconstruction; fused shard reduce / apply /
+# broadcast) on P = 3 local replicas, two iterations
+P = 3
+lc = pos.Context.local_sim(P)
+M, N, K = 130, 264, 8
+Us, Vs = zip(*(si.exact_factors(si.rng(11, 0, p), K, M, N) for p in range(P)))
+W, b = si.exact_weights(si.rng(12), M, N), si.exact_weights(si.rng(13), M)
+Ws, bs = [up(W) for _ in range(P)], [up(b) for _ in range(P)]
+lf = pos.LoopFC(lc, M, N, K, Ws, bs, "bf16")
+for it in range(2):
+    lf.sync([up(u, torch.bfloat16) for u in Us], [up(v, torch.bfloat16) for v in Vs], si.EXACT_ALPHA)
+torch.cuda.synchronize()
+Wr, br = W, b
+for it in range(2):
+    Wr, br = sync.sfb_update(Wr, br, Us, Vs, si.EXACT_ALPHA)
+ok &= all(np.array_equal(x.cpu().numpy().astype(np.float64), Wr) for x in Ws)
+ok &= all(np.array_equal(x.cpu().numpy().astype(np.float64), br) for x in bs)
+lf.close()
+n = 3001
+Pn = pos.pos_padded_size(n, P)
+gs = [si.exact_dense_grad(si.rng(14, 0, p), n) for p in range(P)]
+w = si.exact_weights(si.rng(15), n)
+Gd = [torch.zeros(Pn, device="cuda") for _ in range(P)]
+Wd = [torch.zeros(Pn, device="cuda") for _ in range(P)]
+for p in range(P):
+    Gd[p][:n] = up(gs[p]); Wd[p][:n] = up(w)
+lc.loop_sync_layer_ps(n, Gd, Wd, si.EXACT_ALPHA)
+torch.cuda.synchronize()
+ref = sync.ps_update(w, gs, si.EXACT_ALPHA)
+ok &= all(np.array_equal(x[:n].cpu().numpy().astype(np.float64), ref) for x in Wd)
+lc.close()
+# CTA-pair (cluster) reconstruction on a ragged shape
+os.environ["POS_SFB_PAIR"] = "1"
+c2 = pos.Context.local_sim(2)
+M, N, K = 257, 132, 8
+Us, Vs = zip(*(si.exact_factors(si.rng(16, 0, p), K, M, N) for p in range(2)))
+W, b = si.exact_weights(si.rng(17), M, N), si.exact_weights(si.rng(18), M)
+Wd, bd = up(W), up(b)
+c2.sim_sync_layer_sfb([up(u, torch.bfloat16) for u in Us], [up(v, torch.bfloat16) for v in Vs], Wd, bd, si.EXACT_ALPHA, "bf16")
+torch.cuda.synchronize()
+Wr, br = sync.sfb_update(W, b, Us, Vs, si.EXACT_ALPHA)
+ok &= np.array_equal(Wd.cpu().numpy().astype(np.float64), Wr) and np.array_equal(bd.cpu().numpy().astype(np.float64), br)
+c2.close()
 print("sanitize_small:", "OK" if ok else "MISMATCH")
 sys.exit(0 if ok else 1)
