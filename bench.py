@@ -42,11 +42,11 @@ UNIT = "params/s"
 
 
 def default_bucket_mb(P):
-    """PS unit size of the timed plan (--bucket-mb default). Each fused cross-GPU PS unit costs
-    ~17 us of fixed latency, so fewer, larger units win while the PS chain is exposed: measured on
-    VGG19-22K, 64 MiB at P <= 2 (P = 2: 0.338 vs 0.375 ms with 16 MiB), 16 MiB at P >= 4 (P = 4:
-    0.366 vs 0.412 ms with 64 MiB — there the big unit, issued last, ends the step)."""
-    return 64.0 if P <= 2 else 16.0
+    """PS unit size of the timed plan (--bucket-mb default), as measured on VGG19-22K (round 2):
+    P = 1: 16 MiB (local applies; 64 MiB +0.8%); P = 2: 64 MiB (each fused cross-GPU unit costs
+    ~17 us of fixed latency and the PS chain is exposed: 0.338 vs 0.375 ms with 16 MiB); P >= 4:
+    16 MiB (0.366 vs 0.412 ms with 64 MiB — the big unit, issued last, ends the step)."""
+    return 64.0 if P == 2 else 16.0
 
 
 DEFAULT_BUCKET_MB = default_bucket_mb(1)
@@ -95,7 +95,7 @@ def parse():
     ap.add_argument("--bucket-mb", type=float, default=None,
                     help="PS unit = consecutive dense layers up to this many MiB of fp32 (the paper "
                          "moves PS traffic in 2 MB KV pairs); default default_bucket_mb(P): 64 at "
-                         "P <= 2, 16 at P >= 4; 0 = one unit per layer")
+                         "P = 2, else 16; 0 = one unit per layer")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tf32", action="store_true", help="skip the extra tf32-factor measurement")
