@@ -60,9 +60,11 @@ enum {
   POS_ETIMEOUT = -7   /* a cross-GPU wait exceeded the context's timeout (sticky) */
 };
 /* Summation order of the PS reduce (pos_set_reduce_order). SWITCH: multimem.ld_reduce, the NVSwitch
- * adds the P gradients (its order); RANK_ORDER: every rank loads the P gradients of its shard from
- * its peers and adds them in rank order 0..P-1 — bitwise reproducible run to run. */
-enum { POS_REDUCE_SWITCH = 0, POS_REDUCE_RANK_ORDER = 1 };
+ * adds the P gradients (its order) and multimem.st broadcasts the shard; RANK_ORDER: every rank
+ * loads the P gradients of its shard from its peers and adds them in rank order 0..P-1 — bitwise
+ * reproducible run to run — then multicasts the shard; AUTO (default): at P = 2 rank-order peer loads
+ * with plain peer stores (fewest NVLink bytes at P = 2, deterministic), else SWITCH. */
+enum { POS_REDUCE_SWITCH = 0, POS_REDUCE_RANK_ORDER = 1, POS_REDUCE_AUTO = 2 };
 /* Fault injection (pos_inject_fault; tests of the watchdog):
  *   SKIP_PS  : the given rank does not launch its fused PS kernels (its peers' barriers time out);
  *   SKIP_PACK: loopback only — the given simulated rank does not pack (the flag waits time out). */
@@ -158,7 +160,8 @@ int pos_get_async_error(pos_ctx* ctx);
  * kernel records POS_ETIMEOUT and returns instead of hanging (results of that iteration are
  * undefined; the context is poisoned). 0 = unbounded. Default: env POS_TIMEOUT_MS, else 20000. */
 int pos_set_timeout_ms(pos_ctx* ctx, int64_t ms);
-/* PS reduce order (POS_REDUCE_*); every rank must set the same. Default POS_REDUCE_SWITCH. */
+/* PS reduce order (POS_REDUCE_*); every rank must set the same. Default POS_REDUCE_AUTO (env
+ * POS_REDUCE_ORDER=0|1|2 sets the context default). */
 int pos_set_reduce_order(pos_ctx* ctx, int32_t order);
 /* Fault injection for tests (POS_FAULT_*); rank = the rank that misbehaves. */
 int pos_inject_fault(pos_ctx* ctx, int32_t kind, int32_t rank);

@@ -20,7 +20,7 @@ POS_DT_BF16, POS_DT_TF32, POS_DT_F32 = 0, 1, 2
 POS_IN_BF16, POS_IN_F32 = 0, 1
 POS_OK, POS_EINVAL, POS_ESTATE, POS_ECUDA, POS_ENCCL, POS_ENOMEM, POS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 POS_ETIMEOUT = -7
-POS_REDUCE_SWITCH, POS_REDUCE_RANK_ORDER = 0, 1
+POS_REDUCE_SWITCH, POS_REDUCE_RANK_ORDER, POS_REDUCE_AUTO = 0, 1, 2
 POS_FAULT_NONE, POS_FAULT_SKIP_PS, POS_FAULT_SKIP_PACK = 0, 1, 2
 POS_SCHED_TIMING, POS_SCHED_SEQUENTIAL, POS_SCHED_TIMING_APPLY, POS_SCHED_NO_SYMM, POS_SCHED_PS_AFTER_SFB = 1, 2, 4, 8, 16
 POS_SCHED_STATIC_TILES, POS_SCHED_TRACE = 32, 64
@@ -207,7 +207,8 @@ class Context:
         _chk(lib().pos_set_timeout_ms(self.h, int(ms)), "pos_set_timeout_ms")
 
     def set_reduce_order(self, order: int):
-        """POS_REDUCE_SWITCH (NVLS multimem reduce) or POS_REDUCE_RANK_ORDER (deterministic)."""
+        """POS_REDUCE_SWITCH (NVLS multimem reduce), POS_REDUCE_RANK_ORDER (deterministic) or
+        POS_REDUCE_AUTO (default: rank-order peer loads + peer stores at P = 2, else SWITCH)."""
         _chk(lib().pos_set_reduce_order(self.h, order), "pos_set_reduce_order")
 
     def inject_fault(self, kind: int, rank: int):

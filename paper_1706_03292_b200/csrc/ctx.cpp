@@ -173,8 +173,11 @@ static int ctx_common_init(pos_ctx* c) {
   *h = 0;
   c->err_host = h;
   POS_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), h, 0));
-  // POS_REDUCE_ORDER=1: fixed rank-order reduce in the fused PS kernel (pos_set_reduce_order)
-  if (env_int("POS_REDUCE_ORDER", 0) == 1) c->reduce_order = POS_REDUCE_RANK_ORDER;
+  // POS_REDUCE_ORDER=0|1|2: the context's default PS reduce order (pos_set_reduce_order)
+  {
+    const int64_t o = env_int("POS_REDUCE_ORDER", POS_REDUCE_AUTO);
+    if (o == POS_REDUCE_SWITCH || o == POS_REDUCE_RANK_ORDER || o == POS_REDUCE_AUTO) c->reduce_order = (int)o;
+  }
   const int64_t ms = env_int("POS_TIMEOUT_MS", 20000);
   c->timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
   return POS_OK;
@@ -262,7 +265,8 @@ int pos_set_timeout_ms(pos_ctx* c, int64_t ms) {
 
 int pos_set_reduce_order(pos_ctx* c, int32_t order) {
   clear_error();
-  POS_CHECK_ARG(c && (order == POS_REDUCE_SWITCH || order == POS_REDUCE_RANK_ORDER),
+  POS_CHECK_ARG(c && (order == POS_REDUCE_SWITCH || order == POS_REDUCE_RANK_ORDER ||
+                      order == POS_REDUCE_AUTO),
                 "bad arguments");
   c->reduce_order = order;
   return POS_OK;

@@ -22,7 +22,7 @@ struct pos_ctx {
   volatile int* err_host = nullptr;
   int* err_dev = nullptr;
   unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
-  int reduce_order = POS_REDUCE_SWITCH;   // PS reduce: NVLS switch order or fixed rank order
+  int reduce_order = POS_REDUCE_AUTO;     // PS reduce: NVLS switch order, fixed rank order, auto
   int fault = POS_FAULT_NONE, fault_rank = -1;   // fault injection (tests)
 };
 

@@ -612,16 +612,12 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   // n/2 words per GPU and direction where the switch path moves ~1.5 n. Round 1 kept NVLS (the peer
   // path slowed a co-running reconstruction more); with the PS CTAs now co-resident with the
   // reconstruction and 64 MiB buckets, the peer path wins at P = 2 (round 2: VGG19-22K 0.426 ->
-  // 0.338 ms, Inception-V3 0.296 -> 0.282 ms). POS_PS_P2P=0 selects the NVLS kernel.
-  static const bool p2p2 = [] {
-    const char* e = getenv("POS_PS_P2P");
-    return !(e && e[0] == '0');
-  }();
+  // 0.338 ms, Inception-V3 0.296 -> 0.282 ms): POS_REDUCE_AUTO's choice at P = 2.
   cudaError_t e = cudaSuccess;
   if (c->fault == POS_FAULT_SKIP_PS && c->fault_rank == c->rank) {
     // fault injection: this rank never joins the unit (its peers' entry barriers time out)
-  } else if (P == 2 && p2p2) {
-    e = launch_ps<false, false>(grid, s, a, x);
+  } else if (P == 2 && c->reduce_order == POS_REDUCE_AUTO) {
+    e = launch_ps<false, false>(grid, s, a, x);   // rank-order peer loads, peer stores
   } else if (c->reduce_order == POS_REDUCE_RANK_ORDER) {
     e = launch_ps<false, true>(grid, s, a, x);   // deterministic sum, multicast broadcast
   } else {

@@ -63,13 +63,16 @@ for mb in [1, 4, 16, 64, 256, 1024]:
         Pn = pos.pos_padded_size(n, world)
         Ws, Gs = ctx.sym_empty(Pn), ctx.sym_empty(Pn)
         Gs.normal_()
-        for order, name in ((pos.POS_REDUCE_SWITCH, "nvls"), (pos.POS_REDUCE_RANK_ORDER, "rank_order")):
+        orders = [(pos.POS_REDUCE_SWITCH, "nvls"), (pos.POS_REDUCE_RANK_ORDER, "rank_order")]
+        if world == 2:
+            orders.append((pos.POS_REDUCE_AUTO, "p2p"))   # peer loads + peer stores
+        for order, name in orders:
             ctx.set_reduce_order(order)
             t = timeit(lambda: ctx.sync_layer_ps(n, Gs, Ws, -1e-6))
             # a PS unit = reduce-scatter + all-gather volume: 2 (P-1)/P n 4 bytes per direction
             row[f"ps_{name}_ms"] = t
             row[f"ps_{name}_busbw_gbs"] = 2 * bus(t)
-        ctx.set_reduce_order(pos.POS_REDUCE_SWITCH)
+        ctx.set_reduce_order(pos.POS_REDUCE_AUTO)
     rows.append(row)
     if rank == 0:
         print(json.dumps(row), flush=True)
@@ -83,7 +86,9 @@ if rank == 0:
         "ag_busbw_gbs": max(r["ag_busbw_gbs"] for r in rows),
         "rs_busbw_gbs": max(r["rs_busbw_gbs"] for r in rows),
         # the best per-direction rate any method reached: NCCL AG / RS or the fused PS unit
-        "per_dir_gbs": max(max(r["ag_busbw_gbs"], r["rs_busbw_gbs"], r.get("ps_nvls_busbw_gbs", 0)) for r in rows),
+        "per_dir_gbs": max(max(r["ag_busbw_gbs"], r["rs_busbw_gbs"], r.get("ps_nvls_busbw_gbs", 0),
+                               r.get("ps_p2p_busbw_gbs", 0)) for r in rows),
+        "ps_p2p_busbw_gbs": max(r.get("ps_p2p_busbw_gbs", 0) for r in rows),
         "ps_nvls_busbw_gbs": max(r.get("ps_nvls_busbw_gbs", 0) for r in rows),
         "ps_rank_order_busbw_gbs": max(r.get("ps_rank_order_busbw_gbs", 0) for r in rows),
         "sizes": rows,

@@ -117,7 +117,8 @@ def _worker(rank, world, port, outdir):
         w0 = si.stat_weights(si.rng(96), 1, n)[0]
         Ws, Gs = ctx.sym_empty(Pn), ctx.sym_empty(Pn)
         Gs[:n] = to_dev(gl)
-        for order, name in ((pos.POS_REDUCE_SWITCH, "switch"), (pos.POS_REDUCE_RANK_ORDER, "rank_order")):
+        for order, name in ((pos.POS_REDUCE_SWITCH, "switch"), (pos.POS_REDUCE_RANK_ORDER, "rank_order"),
+                            (pos.POS_REDUCE_AUTO, "auto")):
             ctx.set_reduce_order(order)
             digs = []
             for rep in range(3):
@@ -135,14 +136,16 @@ def _worker(rank, world, port, outdir):
                 g_ = to_host(Ws[:n])
                 check(f"ps_{name}_stat_tol", err(g_, r_) <= 1e-5 and err(g_ - w0, r_ - w0) <= 1e-5)
         check("ps_rank_order_deterministic", res["info"]["ps_rank_order_run_to_run_identical"])
-        ctx.set_reduce_order(pos.POS_REDUCE_SWITCH)
+        if P == 2:   # AUTO at P = 2 is the peer-load kernel: rank order, deterministic too
+            check("ps_auto_p2_deterministic", res["info"]["ps_auto_run_to_run_identical"])
+        ctx.set_reduce_order(pos.POS_REDUCE_AUTO)
 
         # ---- (c) odd sizes incl. n = 16400 (shard lengths differ per rank) -------------------------
         for n_odd in (16400, 1, 130, 590080 + 77):
             Po = pos.pos_padded_size(n_odd, P)
             go = [si.exact_dense_grad(si.rng(97, n_odd % 89, q), n_odd) for q in range(P)]
             wo = si.exact_weights(si.rng(98), n_odd)
-            for order in (pos.POS_REDUCE_SWITCH, pos.POS_REDUCE_RANK_ORDER):
+            for order in (pos.POS_REDUCE_SWITCH, pos.POS_REDUCE_RANK_ORDER, pos.POS_REDUCE_AUTO):
                 ctx.set_reduce_order(order)
                 Wo, Go = ctx.sym_empty(Po), ctx.sym_empty(Po)
                 Wo[:n_odd] = to_dev(wo)
@@ -151,7 +154,7 @@ def _worker(rank, world, port, outdir):
                 ctx.sync_layer_ps(n_odd, Go, Wo, si.EXACT_ALPHA)
                 torch.cuda.synchronize()
                 check(f"ps_exact_{n_odd}_{order}", np.array_equal(to_host(Wo[:n_odd]), sync.ps_update(wo, go, si.EXACT_ALPHA)))
-        ctx.set_reduce_order(pos.POS_REDUCE_SWITCH)
+        ctx.set_reduce_order(pos.POS_REDUCE_AUTO)
         check("no_async_error", ctx.async_error() == pos.POS_OK)
         ctx.close()
 
