@@ -565,6 +565,7 @@ def run_ours(a):
     # which retires the events in eager mode
     has_fc, has_dense = any(u["kind"] == "fc" for u in units), any(u["kind"] == "dense" for u in units)
     traced_ms = None
+    trace_timeline = None
     if a.no_trace:    # CUDA-event timing of the apply stages (events inside the captured step)
         a4_span_ms = sch.timing_span(pos.POS_SCHEME_SFB) if has_fc else None
         ps_span_ms = sch.timing_span(pos.POS_SCHEME_PS) if has_dense else None
@@ -595,6 +596,13 @@ def run_ours(a):
         a4_span_ms = sch.trace_span(pos.POS_SCHEME_SFB)[0] / 1e3 if has_fc else None
         ps_span_ms = sch.trace_span(pos.POS_SCHEME_PS)[0] / 1e3 if has_dense else None
         unit_apply_ms = [sch.trace(un["layers"][0])[0] / 1e3 for un in units]
+        # the last traced step's apply kernels as [first CTA start, last CTA end] (%globaltimer),
+        # relative to the earliest: a timeline with no events on the streams (rank 0's)
+        stamps = [sch.trace_last(un["layers"][0]) for un in units]
+        t0 = min(st for st, _ in stamps)
+        trace_timeline = [[model.layers[un["layers"][0]].name + ("" if len(un["layers"]) == 1 else f"..(+{len(un['layers']) - 1})"),
+                           "SFB" if un["kind"] == "fc" else "PS", round((st - t0) / 1e3, 1), round((en - t0) / 1e3, 1)]
+                          for un, (st, en) in zip(units, stamps)]
         if world > 1:
             t = torch.tensor([traced_ms, a4_span_ms or 0.0, ps_span_ms or 0.0] + unit_apply_ms, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -850,6 +858,7 @@ def run_ours(a):
         "clocks": clk,
         "e2e": e2e,
         "scheme_choice": choice,
+        "trace_timeline_us": trace_timeline,
         "gpu_launches": n_launch * a.steps,
         "gpu_launches_note": "libposeidon kernels per timed region (NCCL kernels and cudaMemsetAsync not counted)",
     }

@@ -354,6 +354,9 @@ int pos_sched_timeline(pos_sched* s, float* out, int32_t max_units);
  * start to last CTA end, %globaltimer) and the number of launches since the last reset. Outputs may
  * be NULL. Synchronises the device. */
 int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, int64_t* launches);
+/* The last traced launch of layer l's unit apply kernel as absolute %globaltimer stamps (ns; first
+ * CTA start, last CTA end) — a timeline of one step without events on the streams. */
+int pos_sched_trace_last(pos_sched* s, int32_t l, int64_t* start_ns, int64_t* end_ns);
 /* The SPAN of all apply kernels of `scheme` within one step (earliest CTA start of the first to the
  * latest CTA end of the last; they overlap on several streams), averaged over steps. POS_ESTATE if
  * the scheme has no traced kernels (e.g. the SIMT f32 path). */

@@ -402,6 +402,12 @@ class Scheduler:
         _chk(lib().pos_sched_trace(self.h, l, C.byref(a), C.byref(b), C.byref(n)), "pos_sched_trace")
         return a.value, b.value, n.value
 
+    def trace_last(self, l):
+        """pos_sched_trace_last: (start_ns, end_ns) %globaltimer stamps of layer l's last traced launch."""
+        a, b = C.c_int64(), C.c_int64()
+        _chk(lib().pos_sched_trace_last(self.h, l, C.byref(a), C.byref(b)), "pos_sched_trace_last")
+        return a.value, b.value
+
     def trace_span(self, scheme=None):
         """pos_sched_trace_span: (average us, steps) of the step's apply-kernel span of `scheme`."""
         a, n = C.c_double(), C.c_int64()

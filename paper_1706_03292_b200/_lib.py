@@ -71,6 +71,7 @@ SIGNATURES = {
     "pos_sched_timeline": (C.c_int, [vp, P_f32, i32]),
     "pos_sched_trace": (C.c_int, [vp, i32, P_f64, P_f64, P_i64]),
     "pos_sched_trace_span": (C.c_int, [vp, i32, P_f64, P_i64]),
+    "pos_sched_trace_last": (C.c_int, [vp, i32, P_i64, P_i64]),
     "pos_sched_trace_reset": (C.c_int, [vp]),
     "pos_sched_set_trace": (C.c_int, [vp, i32]),
     "pos_sched_timing_span": (C.c_int, [vp, i32, P_f32]),

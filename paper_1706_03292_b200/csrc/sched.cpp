@@ -785,6 +785,23 @@ int pos_sched_trace(pos_sched* s, int32_t l, double* avg_us, double* last_us, in
   return read_trace(un.trace, avg_us, last_us, launches);
 }
 
+int pos_sched_trace_last(pos_sched* s, int32_t l, int64_t* start_ns, int64_t* end_ns) {
+  clear_error();
+  int rc = check_layer(s, l);
+  if (rc) return rc;
+  POS_CHECK_ARG(start_ns && end_ns, "NULL output");
+  if (!s->layers[l].added) POS_FAIL(POS_ESTATE, "layer %d not added", l);
+  const Unit& un = s->units[s->layers[l].unit];
+  if (!un.trace) POS_FAIL(POS_ESTATE, "no traced iteration yet");
+  POS_CUDA_TRY(cudaDeviceSynchronize());
+  unsigned long long h[kTraceWords];
+  POS_CUDA_TRY(cudaMemcpy(h, un.trace, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h[3] == 0) POS_FAIL(POS_ESTATE, "no traced launch of layer %d yet", l);
+  *start_ns = (int64_t)h[5];
+  *end_ns = (int64_t)h[6];
+  return POS_OK;
+}
+
 int pos_sched_trace_span(pos_sched* s, int32_t scheme, double* avg_us, int64_t* steps) {
   clear_error();
   POS_CHECK_ARG(s && (scheme == POS_SCHEME_SFB || scheme == POS_SCHEME_PS), "bad arguments");
