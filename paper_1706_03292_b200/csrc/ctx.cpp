@@ -70,13 +70,13 @@ int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W) {
 
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                    cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail, KTrace tr,
-                   KTrace tg) {
+                   KTrace tg, int lane) {
   const int P = c->world;
   const int64_t S = pos_shard_stride(n, P);
   if (S < 0) return (int)S;
   {  // NVLS fused kernel when grad and W live in symmetric memory (NEXT-1)
     bool done = false;
-    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done, tr, tg);
+    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done, tr, tg, lane);
     if (rc != POS_OK || done) return rc;
   }
   const int64_t padded = S * P;
@@ -167,6 +167,10 @@ static int ctx_common_init(pos_ctx* c) {
   int prio = hi;
   if (const char* e = getenv("POS_COMM_PRIO")) prio = std::max(hi, std::min(lo, lo - atoi(e)));
   POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio));
+  c->lane_stream[0] = c->comm_stream;
+  c->ps_lanes = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxLanes, env_int("POS_PS_LANES", 1)));
+  if (c->ps_lanes > 1)
+    POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->lane_stream[1], cudaStreamNonBlocking, prio));
   // watchdog error word: host-mapped, so the host reads it without synchronising
   int* h = nullptr;
   POS_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h), sizeof(int), cudaHostAllocMapped));
@@ -233,6 +237,7 @@ int pos_finalize(pos_ctx* c) {
   if (!c) return POS_OK;
   int rc = POS_OK;
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  if (c->lane_stream[1]) cudaStreamSynchronize(c->lane_stream[1]);
   symm_destroy(c);
   if (c->comm) {
     ncclResult_t r = ncclCommDestroy(c->comm);
@@ -240,6 +245,7 @@ int pos_finalize(pos_ctx* c) {
   }
   if (c->ws) cudaFree(c->ws);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->lane_stream[1]) cudaStreamDestroy(c->lane_stream[1]);
   if (c->err_host) cudaFreeHost(const_cast<int*>(c->err_host));
   delete c;
   return rc;

@@ -12,6 +12,11 @@ struct pos_ctx {
   bool local = false;    // pos_init_local: simulated P, no NCCL
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;  // high-priority stream for collectives (scheduler)
+  // fused PS units may run on up to kMaxLanes concurrent LANES: each lane has its own stream and
+  // its own cross-GPU barrier inbox / epochs, so units of different lanes overlap while each lane
+  // stays stream-ordered (POS_PS_LANES; the scheduler assigns lanes by unit registration order)
+  cudaStream_t lane_stream[2] = {nullptr, nullptr};   // [0] = comm_stream
+  int ps_lanes = 1;
   int max_ctas = 0;
   void* ws = nullptr;    // one-shot workspace (grow-only)
   size_t ws_bytes = 0;
@@ -45,7 +50,7 @@ inline ncclDataType_t nccl_type(int32_t dtype) {
 // and the tail stays zero because the in-place reduce-scatter only ever sums zeros into it).
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                    cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail,
-                   KTrace tr = {}, KTrace tg = {});
+                   KTrace tr = {}, KTrace tg = {}, int lane = 0);
 // grid of the traced kernel stage_ps_dense launches for a unit of n parameters on this rank
 int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W);
 int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
@@ -58,7 +63,8 @@ void symm_destroy(pos_ctx* c);
 // (and nothing enqueued) otherwise
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                   cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr = {},
-                  KTrace tg = {});
+                  KTrace tg = {}, int lane = 0);
+constexpr int kMaxLanes = 2;
 // grid of the fused PS kernel for a unit of n parameters (rank-invariant)
 int symm_ps_grid(pos_ctx* c, int64_t n);
 // pack this rank's factors and multicast them into every rank's gather buffer when the gather

@@ -257,6 +257,9 @@ int issue_unit(pos_sched* s, int ui) {
   // the fused PS kernels, which keep the comm stream to themselves: the PS chain then starts
   // with the first dense unit instead of queueing behind every factor pack of the step
   if (coll && un.scheme == POS_SCHEME_SFB && un.flag_mode && s->pack_stream) cs = s->pool[5];
+  // PS units alternate between the context's lanes by registration order (identical on every rank)
+  const int lane = (coll && un.scheme != POS_SCHEME_SFB && c->ps_lanes > 1) ? un.seq % c->ps_lanes : 0;
+  if (lane > 0) cs = c->lane_stream[lane];
   for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_in, 0));
   // the stage that WRITES W waits for b^l to have finished reading it (WAR)
   const Layer& l0 = s->layers[un.members[0]];
@@ -349,7 +352,7 @@ int issue_unit(pos_sched* s, int ui) {
     if (ts && (rc = trec(ts->packed, cs))) return rc;
     rc = stage_ps_dense(c, un.n, un.grad, un.W, s->alpha, cs, ts ? ts->a0 : nullptr,
                         ts ? ts->a1 : nullptr, /*zero_tail=*/false, unit_trace(s, un),
-                        group_trace(s, POS_SCHEME_PS));
+                        group_trace(s, POS_SCHEME_PS), lane);
     if (rc != POS_OK) return rc;
     if (ts && (rc = trec(ts->done, cs))) return rc;
     POS_CUDA_TRY(cudaEventRecord(un.ev_done, cs));

@@ -397,13 +397,14 @@ int ps_grid(pos_ctx* c, int64_t n, int P) {
   return grid_for(std::max<int64_t>(1, S / 4 / kPsUnroll), kPsThreads, cap);
 }
 
-Xg make_xg(pos_ctx* c, int site) {
+// lane k: inbox pair at byte offset 64 k of the barrier window, epochs at bar_state + 4 k
+Xg make_xg(pos_ctx* c, int site, int lane = 0) {
   Xg x{};
   SymmState* st = state(c);
   if (st && st->bar.mc && c->world > 1) {
-    x.mc = reinterpret_cast<uint32_t*>(st->bar.mc);
-    x.local = reinterpret_cast<uint32_t*>(st->bar.base);
-    x.state = st->bar_state;
+    x.mc = reinterpret_cast<uint32_t*>(st->bar.mc + 64 * lane);
+    x.local = reinterpret_cast<uint32_t*>(st->bar.base + 64 * lane);
+    x.state = st->bar_state + 4 * lane;
   }
   x.P = c->world;
   x.timeout_ns = c->timeout_ns;
@@ -527,8 +528,8 @@ static int symm_init(pos_ctx* c) {
   }
   int rc = register_window(c, st, p, 4096, &st->bar);
   if (rc == POS_OK && (cudaMemset(p, 0, 4096) != cudaSuccess ||
-                       cudaMalloc(&st->bar_state, 4 * sizeof(uint32_t)) != cudaSuccess ||
-                       cudaMemset(st->bar_state, 0, 4 * sizeof(uint32_t)) != cudaSuccess ||
+                       cudaMalloc(&st->bar_state, 4 * kMaxLanes * sizeof(uint32_t)) != cudaSuccess ||
+                       cudaMemset(st->bar_state, 0, 4 * kMaxLanes * sizeof(uint32_t)) != cudaSuccess ||
                        cudaDeviceSynchronize() != cudaSuccess))
     rc = ctx_cuda_fail(c, cudaGetLastError(), "barrier state");
   if (rc != POS_OK) {
@@ -583,7 +584,7 @@ bool symm_lookup(pos_ctx* c, const void* p, size_t bytes) {
 int symm_ps_grid(pos_ctx* c, int64_t n) { return ps_grid(c, n, c->world); }
 
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr, KTrace tg) {
+                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr, KTrace tg, int lane) {
   *done = false;
   const int P = c->world;
   if (P < 2 || c->local) return POS_OK;
@@ -605,7 +606,7 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   a.trace = tr;
   a.group = tg;
   pos_shard_range(n, P, c->rank, &a.lo, &a.hi);
-  const Xg x = make_xg(c, kSitePsEntry);
+  const Xg x = make_xg(c, kSitePsEntry, lane);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
   const int grid = ps_grid(c, n, P);
   // P = 2: plain peer loads (summed in rank order: deterministic) + unicast peer stores move n/2 +
