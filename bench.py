@@ -830,7 +830,10 @@ def run_ours(a):
                                                   peaks["hbm_gbs"] * 1e9, nvl_gbs * 1e9,
                                                   peaks["bf16_tflops"] * 1e12)
         choice.append({"layer": ly.name, "alg1": pos.SCHEME_NAMES[pos.pos_choose_scheme(ly.M, ly.N, K, P)],
-                       "b200_model": pos.SCHEME_NAMES[s_b], "t_sfb_us": t_s * 1e6, "t_ps_us": t_p * 1e6})
+                       "b200_model": pos.SCHEME_NAMES[s_b], "t_sfb_us": t_s * 1e6, "t_ps_us": t_p * 1e6,
+                       "t_adam_us": 1e6 * pos.pos_scheme_time_adam_b200(
+                           ly.M, ly.N, K, P, 2 if a.dtype == "bf16" else 4, peaks["hbm_gbs"] * 1e9, nvl_gbs * 1e9,
+                           peaks["bf16_tflops"] * 1e12)})
     out = {
         "metric": METRIC, "value": P * model.total_params / (ms / 1e3), "unit": UNIT,
         "n_gpus": P, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,

@@ -110,6 +110,17 @@ int pos_choose_scheme2(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P1
  * terms (hbm <= 0 and tc <= 0 with factor_bytes = 4 reproduce Algorithm 1's decision exactly).
  * Outputs may be NULL. Returns POS_SCHEME_SFB if T_SFB <= T_PS else POS_SCHEME_PS; negative on bad
  * arguments. Oracle: oracle/cost.py b200_times. */
+/* The third scheme of Table 1 (Adam: "send SFs to a parameter server shard, then pull back the
+ * whole updated parameter matrices") in the same B200 time model, with the layer's rows
+ * sharded over the P GPUs (rank s owns M/P rows): every rank pushes u[:, rows(s)] and v to each
+ * owner s, the owner reconstructs-and-applies its rows, every rank pulls the other owners' rows:
+ *   T_ADAM = (P-1) K (M/P + N) factor_bytes / nvl + max(8 M N / (P hbm), 2 M N K / tc)
+ *          + (P-1)/P * 4 M N / nvl
+ * Model only (it reports, it does not choose): the fp32 matrix pull costs what the PS all-gather
+ * does, so on NVLink it loses to SFB whenever SFB wins and to PS whenever factors outweigh the
+ * reduce. Oracle: oracle/cost.py b200_time_adam. Negative on bad arguments. */
+int pos_scheme_time_adam_b200(int64_t M, int64_t N, int64_t K, int32_t P, int32_t factor_bytes,
+                              double hbm, double nvl, double tc, double* t_adam);
 int pos_scheme_times_b200(int64_t M, int64_t N, int64_t K, int32_t P, int32_t factor_bytes,
                           double hbm, double nvl, double tc, double* t_sfb, double* t_ps);
 /* Table 1 cost in ELEMENTS as an exact reduced rational num/den (den >= 1).

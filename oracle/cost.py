@@ -114,6 +114,20 @@ def b200_times(M: int, N: int, K: int, P: int, factor_bytes: int = 2, hbm=6551e9
     return t_sfb, t_ps
 
 
+def b200_time_adam(M: int, N: int, K: int, P: int, factor_bytes: int = 2, hbm=6551e9, nvl=770e9,
+                   tc=1644e12):
+    """T_ADAM as an exact Fraction of seconds: Table 1's Adam with the layer's rows
+    sharded over P owners — SF push (u slice + v to every other owner), the owner's
+    reconstruct-and-apply of its M/P rows, matrix pull of the other owners' rows."""
+    def inv(x):
+        return Fraction(0) if not x else 1 / Fraction(x)
+    ihbm, invl, itc = inv(hbm), inv(nvl), inv(tc)
+    push = Fraction((P - 1) * K * factor_bytes) * (Fraction(M, P) + N) * invl
+    apply = max(Fraction(8 * M * N, P) * ihbm, Fraction(2 * M * N * K) * itc)
+    pull = Fraction(4 * (P - 1) * M * N, P) * invl
+    return push + apply + pull
+
+
 def best_scheme_b200(M: int, N: int, K: int, P: int, factor_bytes: int = 2, hbm=6551e9,
                      nvl=770e9, tc=1644e12) -> str:
     t_sfb, t_ps = b200_times(M, N, K, P, factor_bytes, hbm, nvl, tc)

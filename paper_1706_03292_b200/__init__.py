@@ -57,6 +57,15 @@ def pos_scheme_times_b200(M, N, K, P, factor_bytes=2, hbm=6551e9, nvl=770e9, tc=
     return r, a.value, b.value
 
 
+def pos_scheme_time_adam_b200(M, N, K, P, factor_bytes=2, hbm=6551e9, nvl=770e9, tc=1644e12):
+    """Table 1's Adam scheme (SF push to row-sharded owners, matrix pull) in the B200 time model:
+    T_ADAM seconds (include/poseidon.h)."""
+    t = C.c_double()
+    _chk(lib().pos_scheme_time_adam_b200(M, N, K, P, factor_bytes, float(hbm or 0), float(nvl or 0),
+                                         float(tc or 0), C.byref(t)), "pos_scheme_time_adam_b200")
+    return t.value
+
+
 def pos_choose_scheme(M: int, N: int, K: int, P: int) -> int:
     return _chk(lib().pos_choose_scheme(M, N, K, P), "pos_choose_scheme")
 

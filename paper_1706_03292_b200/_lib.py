@@ -24,6 +24,7 @@ SIGNATURES = {
     "pos_shard_stride": (i64, [i64, i32]),
     "pos_shard_range": (C.c_int, [i64, i32, i32, P_i64, P_i64]),
     "pos_scheme_times_b200": (C.c_int, [i64, i64, i64, i32, i32, f64, f64, f64, P_f64, P_f64]),
+    "pos_scheme_time_adam_b200": (C.c_int, [i64, i64, i64, i32, i32, f64, f64, f64, P_f64]),
     "pos_padded_size": (i64, [i64, i32]),
     "pos_factor_row_elems": (i64, [i64, i64]),
     "pos_get_unique_id": (C.c_int, [vp]),

@@ -94,6 +94,21 @@ int pos_scheme_times_b200(int64_t M, int64_t N, int64_t K, int32_t P, int32_t fa
   return sfb <= ps ? POS_SCHEME_SFB : POS_SCHEME_PS;
 }
 
+int pos_scheme_time_adam_b200(int64_t M, int64_t N, int64_t K, int32_t P, int32_t factor_bytes,
+                              double hbm, double nvl, double tc, double* t_adam) {
+  clear_error();
+  POS_CHECK_ARG(M >= 1 && N >= 1 && K >= 1 && P >= 1, "M, N, K, P must be >= 1");
+  POS_CHECK_ARG(factor_bytes == 2 || factor_bytes == 4, "factor_bytes must be 2 or 4");
+  POS_CHECK_ARG(t_adam, "NULL output");
+  const double m = (double)M, n = (double)N, k = (double)K, p = (double)P;
+  const double ihbm = hbm > 0 ? 1.0 / hbm : 0.0, invl = nvl > 0 ? 1.0 / nvl : 0.0,
+               itc = tc > 0 ? 1.0 / tc : 0.0;
+  const double a_hbm = 8.0 * m * n / p * ihbm, a_tc = 2.0 * m * n * k * itc;
+  *t_adam = (p - 1) * k * (m / p + n) * factor_bytes * invl + (a_hbm > a_tc ? a_hbm : a_tc) +
+            4.0 * (p - 1) * m * n / p * invl;
+  return POS_OK;
+}
+
 // Table 1, as exact reduced rationals.
 int pos_cost_elems(int32_t scheme, int32_t role, int64_t M, int64_t N, int64_t K, int32_t P1,
                    int32_t P2, uint64_t* num, uint64_t* den) {

@@ -113,7 +113,8 @@ for (M, N, K) in SHAPES:
     s_b, m_sfb, m_ps = pos.pos_scheme_times_b200(M, N, K, P)
     row = {"M": M, "N": N, "K": K, "P": P, "t_sfb_us": t_sfb, "t_ps_us": t_ps,
            "measured": "SFB" if t_sfb <= t_ps else "PS", "alg1": alg1,
-           "b200_model": pos.SCHEME_NAMES[s_b], "model_sfb_us": m_sfb * 1e6, "model_ps_us": m_ps * 1e6}
+           "b200_model": pos.SCHEME_NAMES[s_b], "model_sfb_us": m_sfb * 1e6, "model_ps_us": m_ps * 1e6,
+           "model_adam_us": pos.pos_scheme_time_adam_b200(M, N, K, P) * 1e6}
     rows.append(row)
     if rank == 0:
         print(json.dumps(row), flush=True)

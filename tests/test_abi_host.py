@@ -148,3 +148,14 @@ def test_b200_time_model_reproduces_algorithm_1():
                 for P in range(1, 9):
                     s, _, _ = pos.pos_scheme_times_b200(M, N, K, P, 4, 0, 1.0, 0)
                     assert s == lib.pos_choose_scheme(M, N, K, P), (M, N, K, P)
+
+
+def test_adam_time_model_matches_oracle():
+    """Table 1's third scheme in the B200 model: C (double) equals the oracle's exact Fraction."""
+    for (M, N, K) in [(4096, 4096, 32), (4096, 25088, 32), (1000, 1024, 128), (7, 3, 5), (64, 64, 8)]:
+        for P in (1, 2, 3, 4, 8):
+            for fb in (2, 4):
+                for (hbm, nvl, tc) in [(6551e9, 770e9, 1644e12), (None, 1.0, None), (6551e9, None, None)]:
+                    t = pos.pos_scheme_time_adam_b200(M, N, K, P, fb, hbm, nvl, tc)
+                    e = cost.b200_time_adam(M, N, K, P, fb, hbm, nvl, tc)
+                    assert abs(t - float(e)) <= 1e-12 * float(e) + 1e-30, (M, N, K, P, fb)

@@ -240,3 +240,42 @@ def test_b200_model_tensor_term_pinned_to_an_independent_flop_count():
             assert t_sfb == t_tc            # tensor-bound regime
         else:
             assert t_sfb == t_hbm
+
+
+def _adam_bytes_by_enumeration(M, N, K, P, fb):
+    """Sharded Adam, transfer by transfer (PAPER:185 'send SFs to a parameter server shard, then
+    pull back the whole updated parameter matrices'), rows split into P contiguous equal blocks:
+    worker w sends its u rows restricted to owner s's rows and its whole v to every owner s != w;
+    owner s sends its W rows (fp32) to every worker w != s. Returns the max over ranks of the bytes
+    each rank RECEIVES (the per-direction NVLink volume the model charges)."""
+    assert M % P == 0
+    rows = M // P
+    recv = [0] * P
+    for w in range(P):
+        for s in range(P):
+            if s == w:
+                continue
+            recv[s] += K * rows * fb + K * N * fb      # SF push: u[:, rows(s)] and v
+            recv[w] += rows * N * 4                    # matrix pull: W[rows(s), :]
+    return max(recv)
+
+
+def test_adam_model_pinned_to_transfer_enumeration_and_p1():
+    """b200_time_adam: the network term equals the enumerated transfers of the sharded protocol
+    (unit bandwidth, no HBM / tensor terms); the apply term equals the owner's share of the
+    in-place update (8 bytes per element of its M/P rows); at P = 1 the model is the local
+    reconstruct-and-apply, identical to SFB's time."""
+    for M in (4, 8, 12):
+        for N in (1, 3, 5):
+            for K in (1, 2, 7):
+                for P in (1, 2, 4):
+                    if M % P:
+                        continue
+                    for fb in (2, 4):
+                        net = cost.b200_time_adam(M, N, K, P, fb, hbm=None, nvl=1, tc=None)
+                        assert net == _adam_bytes_by_enumeration(M, N, K, P, fb), (M, N, K, P, fb)
+                        app = cost.b200_time_adam(M, N, K, P, fb, hbm=1, nvl=None, tc=None)
+                        assert app == Fraction(sum(8 * N for _ in range(M // P)))
+    for (M, N, K) in [(4096, 4096, 32), (1000, 1024, 128)]:
+        t_sfb, _ = cost.b200_times(M, N, K, 1)
+        assert cost.b200_time_adam(M, N, K, 1) == t_sfb
