@@ -46,16 +46,17 @@ def _nvml_handle():
 h = _nvml_handle()
 
 
+_LINKS = list(range(pynvml.NVML_NVLINK_MAX_LINKS))
+
+
 def counters():
-    """(tx KiB, rx KiB) summed over all links."""
-    vals = pynvml.nvmlDeviceGetFieldValues(h, [pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
-                                               pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
-    out = []
-    for v in vals:
-        if v.nvmlReturn != 0:
-            raise RuntimeError(f"NVML field value error {v.nvmlReturn}")
-        out.append(v.value.ullVal)
-    return out
+    """(tx KiB, rx KiB) summed over the links that report (scopeId = link)."""
+    q = [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l) for l in _LINKS] + \
+        [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l) for l in _LINKS]
+    vals = pynvml.nvmlDeviceGetFieldValues(h, q)
+    tx = sum(v.value.ullVal for v in vals[:len(_LINKS)] if v.nvmlReturn == 0)
+    rx = sum(v.value.ullVal for v in vals[len(_LINKS):] if v.nvmlReturn == 0)
+    return tx, rx
 
 
 def measure(fn, iters):
