@@ -116,7 +116,7 @@ def oracle_model(model, host, n_iter, alpha, others=()):
     return ref
 
 
-@pytest.mark.parametrize("bucket_mb", [None, 16.0, 0.0])   # bench default; 16 MiB; one unit per layer
+@pytest.mark.parametrize("bucket_mb", [None, 64.0, 0.0])   # bench default (16 MiB at P = 1); 64 MiB; one unit per layer
 def test_vgg19_22k_bench_step_graph_ring_exact_bitwise(bucket_mb):
     model, host, got, n_iter, alpha = run_model("c3", "exact", bucket_mb=bucket_mb)
     assert model.total_params == 229052817 and len(model.layers) == 19
