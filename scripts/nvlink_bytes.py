@@ -54,6 +54,9 @@ def counters():
     q = [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l) for l in _LINKS] + \
         [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l) for l in _LINKS]
     vals = pynvml.nvmlDeviceGetFieldValues(h, q)
+    if not any(v.nvmlReturn == 0 for v in vals):
+        # the round-2 pool reports NOT_SUPPORTED here (nvidia-smi nvlink -gt d: N/A on every link)
+        raise RuntimeError("NVLink throughput counters are not supported on this system")
     tx = sum(v.value.ullVal for v in vals[:len(_LINKS)] if v.nvmlReturn == 0)
     rx = sum(v.value.ullVal for v in vals[len(_LINKS):] if v.nvmlReturn == 0)
     return tx, rx
