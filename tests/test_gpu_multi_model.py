@@ -67,48 +67,58 @@ def _worker(rank, world, port, outdir):
     try:
         ctx = pos.Context.from_torch_distributed()
         # ---- (a) full VGG19-22K, bench step, graph ring, exact regime ----------------------------
-        model_name, K = si.CONFIGS["c3"]
-        model = si.load_model(model_name)
-        units = bench.plan_units(model, int(bench.default_bucket_mb(P) * 2 ** 20 / 4))
-        sch = pos.Scheduler(ctx, len(model.layers), timing="apply")
-        fill = HostFill("exact", K, rank=rank)
-        bufs = bench.register_units(pos, ctx, sch, model, units, K, "bf16", fill)
-        a = si.EXACT_ALPHA
-        main = torch.cuda.current_stream()
-        step = bench.make_step(sch, bufs, a)
-        torch.cuda.synchronize()
-        dist.barrier(device_ids=[rank])
-        for _ in range(3):
-            step(main)
-        ring = bench.capture_ring(step, main)
-        for g in ring:
-            g.replay()
-        n_iter = 3 + len(ring)
-        torch.cuda.synchronize()
-        res["digests"]["vgg19_22k"] = "".join(_digest(bb["W"]) for bb in bufs)
-        if rank == 0:
-            others = []
-            for q in range(1, P):
-                o = {}
+        def full_model(ctx, key):
+            model_name, K = si.CONFIGS["c3"]
+            model = si.load_model(model_name)
+            units = bench.plan_units(model, int(bench.default_bucket_mb(P) * 2 ** 20 / 4))
+            sch = pos.Scheduler(ctx, len(model.layers), timing="apply")
+            fill = HostFill("exact", K, rank=rank)
+            bufs = bench.register_units(pos, ctx, sch, model, units, K, "bf16", fill)
+            a = si.EXACT_ALPHA
+            main = torch.cuda.current_stream()
+            step = bench.make_step(sch, bufs, a)
+            torch.cuda.synchronize()
+            dist.barrier(device_ids=[rank])
+            for _ in range(3):
+                step(main)
+            ring = bench.capture_ring(step, main)
+            for g in ring:
+                g.replay()
+            n_iter = 3 + len(ring)
+            torch.cuda.synchronize()
+            res["digests"][key] = "".join(_digest(bb["W"]) for bb in bufs)
+            if rank == 0:
+                others = []
+                for q in range(1, P):
+                    o = {}
+                    for l, ly in enumerate(model.layers):
+                        if ly.kind == "fc":
+                            o[(l, "u")] = fill.value("fc", l, (K, ly.M), "u", q)
+                            o[(l, "v")] = fill.value("fc", l, (K, ly.N), "v", q)
+                        else:
+                            o[(l, "g")] = fill.value("dense", l, (ly.n,), "g", q)
+                    others.append(o)
+                ref = oracle_model(model, fill.host, n_iter, a, others)
+                bad = []
                 for l, ly in enumerate(model.layers):
-                    if ly.kind == "fc":
-                        o[(l, "u")] = fill.value("fc", l, (K, ly.M), "u", q)
-                        o[(l, "v")] = fill.value("fc", l, (K, ly.N), "v", q)
-                    else:
-                        o[(l, "g")] = fill.value("dense", l, (ly.n,), "g", q)
-                others.append(o)
-            ref = oracle_model(model, fill.host, n_iter, a, others)
-            bad = []
-            for l, ly in enumerate(model.layers):
-                got = to_host(bufs[l]["W"]).reshape(ref[l][0].shape)
-                if not np.array_equal(got, ref[l][0]):
-                    bad.append(ly.name)
-                if ref[l][1] is not None and not np.array_equal(to_host(bufs[l]["b"]), ref[l][1]):
-                    bad.append(ly.name + ".bias")
-            res["info"]["vgg19_22k_bad_layers"] = bad
-            check("vgg19_22k_graph_ring_exact_oracle", not bad)
-        ring = None
-        sch.close()
+                    got = to_host(bufs[l]["W"]).reshape(ref[l][0].shape)
+                    if not np.array_equal(got, ref[l][0]):
+                        bad.append(ly.name)
+                    if ref[l][1] is not None and not np.array_equal(to_host(bufs[l]["b"]), ref[l][1]):
+                        bad.append(ly.name + ".bias")
+                res["info"][key + "_bad_layers"] = bad
+                check(key + "_graph_ring_exact_oracle", not bad)
+            ring = None
+            sch.close()
+        full_model(ctx, "vgg19_22k")
+        # the same with the fused PS units on two lanes (own streams and barrier epochs)
+        os.environ["POS_PS_LANES"] = "2"
+        try:
+            ctx_l = pos.Context.from_torch_distributed()
+        finally:
+            del os.environ["POS_PS_LANES"]
+        full_model(ctx_l, "vgg19_22k_lanes2")
+        ctx_l.close()
 
         # ---- (b) PS determinism: switch order (recorded) and rank order (asserted) ----------------
         n = 2359808 * 4 + 4097
