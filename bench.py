@@ -766,8 +766,13 @@ def run_ours(a):
     t_pipe, t_seq, t_nvl, t_kern = roofline_times(rows, peaks, P, nvl_gbs)
     a4_bytes = sum(r["hbm_a4"] for r in rows)
     a4_flop = sum(r["flop_a4"] for r in rows)
+    # per-launch basis (the contract's "bytes per launch / average launch duration"): algorithmic
+    # bytes of the step's reconstructions over the sum of their launch durations (first CTA start to
+    # last CTA end of each launch); the span of all of them (they overlap on two streams) is kept
+    # beside it
+    n_a4 = sum(1 for r in rows if r["scheme"] == "SFB")
     a4_ms_sum = sum(unit_apply_ms[i] for i, r in enumerate(rows) if r["scheme"] == "SFB")
-    a4_ms = a4_span_ms if a4_span_ms else a4_ms_sum
+    a4_ms = a4_ms_sum if a4_ms_sum else (a4_span_ms or 0.0)
     ps_bytes = sum(r["hbm_other"] for r in rows if r["scheme"] == "PS")
     ps_ms = sum(unit_apply_ms[i] for i, r in enumerate(rows) if r["scheme"] == "PS")
     traffic = None
@@ -779,17 +784,22 @@ def run_ours(a):
         if key in tj:
             traffic = tj[key].get("a4_dram_bytes_per_step")
     achieved = a4_bytes / (a4_ms / 1e3) / 1e9 if a4_ms > 0 else None
+    span_achieved = a4_bytes / (a4_span_ms / 1e3) / 1e9 if a4_span_ms else None
     roof = {"kernel": "sfb_tc_kernel (A4 reconstruct-and-apply, all SFB layers of one step)",
             "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic,
             "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
-            "kernel_ms_note": "device-side trace (%%globaltimer stamped by the kernels, no events in "
-                              "the captured step) of a replay of the same step right after the "
-                              "(untraced) timed region, as many steps, averaged: span from the first "
-                              "reconstruction CTA's start to the last one's end in a step (consecutive "
-                              "layers' reconstructions overlap on two streams); sum of per-layer "
-                              "durations: %.4f ms" % a4_ms_sum,
+            "launches_per_step": n_a4, "avg_launch_ms": a4_ms / n_a4 if n_a4 else None,
+            "kernel_ms_note": "per-launch durations from the device-side trace (%globaltimer stamped by "
+                              "the kernels: first CTA start to last CTA end; no events in the captured "
+                              "step) of a replay of the same step right after the (untraced) timed "
+                              "region, as many steps, averaged and summed over the step's launches; "
+                              "achieved = algorithmic bytes of those launches / that sum",
+            "span_ms": a4_span_ms, "span_achieved": span_achieved,
+            "span_frac": span_achieved / peaks["hbm_gbs"] if span_achieved else None,
+            "span_note": "first reconstruction CTA start to last one's end in a step (consecutive layers' "
+                         "reconstructions overlap on two streams; PS applies share HBM inside it)",
             "traced_ms_per_step": traced_ms,
             "per_layer_ms": {model.layers[un["layers"][0]].name: unit_apply_ms[i]
                              for i, un in enumerate(units) if un["kind"] == "fc"},
