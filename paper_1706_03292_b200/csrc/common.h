@@ -234,8 +234,6 @@ struct SfbTcPlan {
   int nb_n = 0, num_tiles = 0, nkb = 0, grid = 0;
   bool tf32 = false;
   bool pair = false;       // CTA-pair kernel (cta_group::2, 256-row tiles) — large K*P
-  bool mc = false;         // 4-CTA clusters: two pairs, V boxes multicast (512-row tiles)
-  bool wide = false;       // wide CTA-pair tile (256 x 512, one TMEM accumulator)
   // device scratch (2 x u32, zero-initialised, owned by the plan's creator) for the dynamic tile
   // scheduler; nullptr = static round-robin tiles. Launches sharing a counter must not overlap.
   unsigned int* counter = nullptr;

@@ -27,10 +27,10 @@
 //    where the operand stream, not W, is the bound. At K*P = 1024 the kernel is bound by the
 //    bytes each SM can keep in flight from L2 (operands 16 B + W 4 B per output element; the
 //    diagnostic builds POS_SFB_EXP show MMA+operands alone at 0.95 of the tensor peak and the W
-//    path alone at 0.92 of HBM — DESIGN.md §10). Rejected variants kept as compile-time options:
-//    4-CTA clusters with TMA multicast of V (POS_SFB_MC; only 33 clusters of 4 co-reside = 132
-//    SMs), a 256 x 512 pair tile with one TMEM accumulator (POS_SFB_WIDE; loses the epilogue /
-//    MMA overlap), a dedicated W storer thread (POS_SFB_STORER).
+//    path alone at 0.92 of HBM — DESIGN.md §11). Measured and removed (round 2, commits 6664201,
+//    7a655b0, 5d59ca3): 4-CTA clusters multicasting V (only 33 clusters of 4 co-reside = 132 SMs:
+//    -8%), a 256 x 512 pair tile with one TMEM accumulator (loses the epilogue / MMA overlap:
+//    -13%), a dedicated W-storer thread (-4% at K*P = 32).
 //
 // Warp roles (256 threads): w0 operand TMA producer, w1 MMA issuer + TMEM owner, w2 W TMA
 // producer, w3 idle, w4..w7 epilogue (warp w%4 owns TMEM lanes 32*(w%4) .. +31 = tile rows).
@@ -79,12 +79,6 @@ constexpr int TR = 4;               // tile-index ring depth (dynamic tile sched
 #ifndef POS_SFB_PSTAGES
 #define POS_SFB_PSTAGES 5   // round 2: 5 stages + 4 W slots beat 4 + 5 at K*P >= 1024 (83 -> 79.5 us, AlexNet fc6)
 #endif
-// W store issue: 0 = epilogue thread 0 issues the TMA store of a sub-tile and retires the slot one
-// sub-tile later; 1 = a dedicated storer thread (warp 3) issues the stores and frees each slot as
-// soon as its store has read shared memory (the epilogue never waits on a store)
-#ifndef POS_SFB_STORER
-#define POS_SFB_STORER 0
-#endif
 // Diagnostics only (never in the shipped build): 1 = no W traffic in the epilogue, 2 = no MMAs,
 // 3 = no MMAs and no operand loads.
 #ifndef POS_SFB_EXP
@@ -102,31 +96,19 @@ constexpr int TR = 4;               // tile-index ring depth (dynamic tile sched
 // computes a 256 x BN tile, each CTA holds its 128 rows of U and HALF of the tile's V columns,
 // so a stage is 2/3 the size and more stages fit — the large-K*P shapes are bound by operand
 // bytes in flight, not by W.
-// kWide (with kPair): the pair's tile is 256 x 2BN — two N = BN MMAs per k step into the two
-// halves of TMEM (one accumulator, no double buffering): 1/4 less operand bytes per output than
-// the 256 x BN tile, for the large-K*P shapes that are bound by L2 -> SM operand bytes.
-#ifndef POS_SFB_WSTAGES
-#define POS_SFB_WSTAGES 4
-#endif
-#ifndef POS_SFB_WWSLOTS
-#define POS_SFB_WWSLOTS 2
-#endif
-template <bool kPair, bool kWide = false>
+template <bool kPair>
 struct Lay {
-  static_assert(!kWide || kPair, "the wide tile is a CTA-pair tile");
-  static constexpr int kStages = kWide ? POS_SFB_WSTAGES : (kPair ? POS_SFB_PSTAGES : POS_SFB_STAGES);
-  static constexpr int kBCols = (kPair && !kWide) ? BN / 2 : BN;   // V columns held per CTA
+  static constexpr int kStages = kPair ? POS_SFB_PSTAGES : POS_SFB_STAGES;
+  static constexpr int kBCols = kPair ? BN / 2 : BN;          // V columns held per CTA
   static constexpr int kBBytes = KBYTES * kBCols;
   static constexpr int kStageBytes = A_BYTES + kBBytes;
-  static constexpr int kWSlots =                                   // W sub-tile ring depth
-      kWide ? POS_SFB_WWSLOTS : (kPair ? POS_SFB_PWSLOTS : POS_SFB_WSLOTS);
-  static constexpr int kEpi = kPair ? POS_SFB_PEPI : POS_SFB_EPI;   // epilogue warpgroups
-  static constexpr int kTN = kWide ? 2 * BN : BN;                   // tile columns
-  static constexpr int kAcc = kWide ? 1 : 2;                        // TMEM accumulators
+  static constexpr int kWSlots = kPair ? POS_SFB_PWSLOTS : POS_SFB_WSLOTS;   // W sub-tile ring depth
+  static constexpr int kEpi = kPair ? POS_SFB_PEPI : POS_SFB_EPI;             // epilogue warpgroups
   static constexpr int kThreads = 128 + 128 * kEpi;
   static constexpr int kData = kStages * kStageBytes + kWSlots * W_BYTES;
-  static constexpr int kBars = 8 * (2 * kStages + 3 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
+  static constexpr int kBars = 8 * (2 * kStages + 2 * kWSlots + 4 + 2 * TR) + 16 + 4 * TR;
   static constexpr int kTotal = kData + kBars + 1024;         // + alignment slack
+  static constexpr int kTileRows = kPair ? 2 * BM : BM;       // W rows per tile
 };
 constexpr int STAGE_BYTES = Lay<false>::kStageBytes;
 constexpr int SMEM_TOTAL = Lay<false>::kTotal;
@@ -134,7 +116,6 @@ constexpr int TMEM_COLS = 2 * BN;
 
 static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 static_assert(Lay<true>::kTotal <= 232448, "shared memory budget (CTA pair)");
-static_assert(Lay<true, true>::kTotal <= 232448, "shared memory budget (wide CTA pair)");
 // A W slot must always be consumed by the same epilogue group: a group waits on a slot's full
 // barrier by phase parity, which is only sound if it consumed the slot's previous phase itself.
 static_assert(Lay<false>::kWSlots % Lay<false>::kEpi == 0 && Lay<true>::kWSlots % Lay<true>::kEpi == 0,
@@ -243,11 +224,11 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t adesc, uint64_t b
 // mbarrier arrives when all previously issued tcgen05 ops of this thread have completed
 // (kPair: on the barrier at this offset in BOTH CTAs of the pair)
 template <bool kPair>
-__device__ __forceinline__ void umma_commit(uint32_t bar, uint16_t mask = 0x3) {
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
   if constexpr (kPair) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(bar), "h"(mask)
+        " [%0], %1;" ::"r"(bar), "h"((uint16_t)0x3)
         : "memory");
   } else {
     asm volatile(
@@ -313,17 +294,6 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
       : "memory");
 }
-// Same, multicast: the box lands at `dst` in every CTA of `mask`; each destination's bytes complete
-// on the barrier at the same offset in the leader (even CTA) of the destination's pair
-__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap* map, uint32_t leader_bar,
-                                                    uint32_t dst, int32_t c0, int32_t c1,
-                                                    uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar), "h"(mask)
-      : "memory");
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -365,11 +335,10 @@ __host__ __device__ constexpr uint32_t instr_desc() {
          ((uint32_t)((kPair ? 2 * BM : BM) >> 4) << 24);
 }
 
-// number of W sub-tiles of a tile of TN columns starting at column n0 that intersect [0, N)
-template <int TN>
+// number of W sub-tiles of the tile starting at column n0 that intersect [0, N)
 __device__ __forceinline__ int nsub_of(int64_t N, int n0) {
   const int64_t s = (N - n0 + WSUB - 1) / WSUB;
-  return s < TN / WSUB ? (int)s : TN / WSUB;
+  return s < NSUB ? (int)s : NSUB;
 }
 
 struct TileInfo {
@@ -386,21 +355,13 @@ struct TileInfo {
   KTrace trace, group;    // device-side launch trace (off when rec == nullptr)
 };
 
-// kMc (with kPair): cluster of 4 = two CTA pairs stacked along m (a 512 x BN tile); both pairs
-// need the same V columns, so each V box is loaded once and multicast to the two CTAs that hold it
-// — 1/4 less operand traffic through L2 than two independent pairs (the large-K*P shapes are bound
-// by L2 -> SM operand bytes).
-template <bool kTF32, bool kPair, bool kMc = false, bool kWide = false>
-__global__ void __launch_bounds__(Lay<kPair, kWide>::kThreads, 1)
+template <bool kTF32, bool kPair>
+__global__ void __launch_bounds__(Lay<kPair>::kThreads, 1)
 sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA2,
               const __grid_constant__ CUtensorMap tmB2, TileInfo ti, float alpha, int accumulate) {
-  using L = Lay<kPair, kWide>;
-  static_assert(!(kMc && kWide), "one large-K*P variant at a time");
+  using L = Lay<kPair>;
   constexpr int ST = L::kStages;             // operand ring depth
-  constexpr int TN = L::kTN, NACC = L::kAcc;
-  // V columns per CTA come in `kHalves` groups of kBH (wide pair: one group per MMA half)
-  constexpr int kHalves = kWide ? 2 : 1, kBH = L::kBCols / kHalves;
   constexpr int EB = kTF32 ? 4 : 2;          // element bytes
   constexpr int BK = KBYTES / EB;            // k rows per stage (64 bf16 / 32 tf32 at 128 B)
   constexpr int CHUNK = SWZ / EB;            // elements per 128-byte chunk along m / n
@@ -409,13 +370,9 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   constexpr uint32_t IDESC = instr_desc<kTF32, kPair>();
   constexpr int WSLOTS = L::kWSlots, EPI = L::kEpi;
   // epilogue warps that must drain an accumulator before the MMA may overwrite it
-  static_assert(!kMc || kPair, "multicast clusters are made of CTA pairs");
-  constexpr int kCl = kMc ? 4 : (kPair ? 2 : 1);   // CTAs per cluster (scheduling unit)
-  constexpr int kTileRows = kCl * BM;               // W rows per (cluster) tile
   constexpr int kDrainers = 4 * EPI * (kPair ? 2 : 1);
   // tile-ring consumers: (MMA issuer | peer operand producer) + W producer + epilogue, per CTA
-  // (kMc: the second pair's leader is both an MMA issuer and a ring-reading operand producer)
-  constexpr int kRingConsumers = (2 + 128 * EPI + (POS_SFB_STORER ? 1 : 0)) * kCl + (kMc ? 1 : 0);
+  constexpr int kRingConsumers = (2 + 128 * EPI) * (kPair ? 2 : 1);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -427,16 +384,13 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const uint32_t b_wfull = b_empty + 8 * ST, b_wempty = b_wfull + 8 * WSLOTS;
   const uint32_t b_tfull = b_wempty + 8 * WSLOTS, b_tempty = b_tfull + 16;
   const uint32_t b_rfull = b_tempty + 16, b_rempty = b_rfull + 8 * TR;   // tile-index ring
-  const uint32_t b_wupd = b_rempty + 8 * TR;   // W slot updated by the epilogue (storer mode)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 3 * WSLOTS + 4 + 2 * TR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 2 * WSLOTS + 4 + 2 * TR);
   volatile int* tile_ring = reinterpret_cast<volatile int*>(tmem_slot + 4);
   const bool dyn = ti.counter != nullptr;
   // CTA pair: the even CTA (rank 0) fetches tiles, issues the MMAs and owns the shared
   // barriers (full, tempty, rempty); each CTA loads and updates its own 128 rows.
   const uint32_t crank = kPair ? cluster_rank() : 0;
-  const uint32_t prank = crank & 1u, pbase = crank & ~1u;   // rank within the pair, pair leader
-  const bool leader = prank == 0;                           // pair leader: issues the MMAs
-  const bool fetcher = crank == 0;                          // cluster leader: fetches the tiles
+  const bool leader = crank == 0;
   const int unit = kPair ? (int)cluster_id_x() : (int)blockIdx.x;   // scheduling unit
   const int nunits = kPair ? (int)nclusters_x() : (int)gridDim.x;
   auto wait_ring = [&](uint32_t bar, uint32_t parity) {
@@ -463,13 +417,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   ktrace_begin(ti.group);
 
   if (threadIdx.x == 0) {
-    // kMc: a stage is free only when BOTH pairs' MMAs have read it (its V boxes were multicast)
-    for (int i = 0; i < ST; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, kMc ? 2 : 1); }
-    for (int i = 0; i < WSLOTS; ++i) {
-      mbar_init(b_wfull + 8 * i, 1);
-      mbar_init(b_wempty + 8 * i, 1);
-      mbar_init(b_wupd + 8 * i, 1);
-    }
+    for (int i = 0; i < ST; ++i) { mbar_init(b_full + 8 * i, 1); mbar_init(b_empty + 8 * i, 1); }
+    for (int i = 0; i < WSLOTS; ++i) { mbar_init(b_wfull + 8 * i, 1); mbar_init(b_wempty + 8 * i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(b_tfull + 8 * i, 1);
       mbar_init(b_tempty + 8 * i, kDrainers);
@@ -519,7 +468,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (!dyn) {
           t = unit + it * nunits;
           if (t >= ti.num_tiles) break;
-        } else if (kPair && !fetcher) {
+        } else if (kPair && !leader) {
           t = tile_of(it, rphase);
           if (t < 0) break;
         } else {   // fetch the next tile and publish it to the other roles (and the peer CTA)
@@ -529,11 +478,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           if (t >= ti.num_tiles) t = -1;
           tile_ring[slot] = t;
           if constexpr (kPair) {
-#pragma unroll
-            for (int q = 1; q < kCl; ++q) {
-              st_cluster_u32(map_rank(smem_u32((const void*)&tile_ring[slot]), q), (uint32_t)t);
-              mbar_arrive_cluster(map_rank(b_rfull + 8 * slot, q));
-            }
+            st_cluster_u32(map_rank(smem_u32((const void*)&tile_ring[slot]), 1), (uint32_t)t);
+            mbar_arrive_cluster(map_rank(b_rfull + 8 * slot, 1));
           }
           mbar_arrive(b_rfull + 8 * slot);
           if (slot == TR - 1) rphase ^= 1;
@@ -547,9 +493,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             break;
           }
         }
-        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM;
-        // this CTA's V columns: half h of the tile starts at n0 + h * BN; the pair splits each half
-        const int nb0 = (t % ti.nb_n) * TN + (int)prank * kBH;
+        const int m0 = (t / ti.nb_n) * L::kTileRows + (int)crank * BM;
+        const int nb0 = (t % ti.nb_n) * BN + (int)crank * L::kBCols;   // this CTA's V columns
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(b_empty + 8 * stage, phase ^ 1);
           const uint32_t sA = sbase + stage * L::kStageBytes, sB = sA + A_BYTES;
@@ -557,27 +502,15 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           if (POS_SFB_EXP == 3) {   // diagnostic: no operand traffic (and no MMAs)
             if (!kPair || leader) mbar_arrive(b_full + 8 * stage);
           } else if constexpr (kPair) {
-            // both CTAs' bytes complete on the pair leader's full barrier
-            const uint32_t full = map_rank(b_full + 8 * stage, pbase);
+            // both CTAs' bytes complete on the leader's full barrier
+            const uint32_t full = map_rank(b_full + 8 * stage, 0);
             if (leader) mbar_expect_tx(b_full + 8 * stage, 2 * L::kStageBytes);
 #pragma unroll
             for (int c = 0; c < BM / CHUNK; ++c)
               tma_load_2d_pair(mA, full, sA + c * BOX_BYTES, m0 + c * CHUNK, k0);
-            if constexpr (kMc) {
-              // V boxes: CTA r of pair p loads the boxes c = p (mod 2) of its column half, for
-              // itself and for CTA r of the other pair
-              const uint16_t mask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
 #pragma unroll
-              for (int c = (int)(crank >> 1); c < L::kBCols / CHUNK; c += 2)
-                tma_load_2d_pair_mc(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0, mask);
-            } else {
-#pragma unroll
-              for (int h = 0; h < kHalves; ++h)
-#pragma unroll
-                for (int c = 0; c < kBH / CHUNK; ++c)
-                  tma_load_2d_pair(mB, full, sB + (h * (kBH / CHUNK) + c) * BOX_BYTES,
-                                   nb0 + h * BN + c * CHUNK, k0);
-            }
+            for (int c = 0; c < L::kBCols / CHUNK; ++c)
+              tma_load_2d_pair(mB, full, sB + c * BOX_BYTES, nb0 + c * CHUNK, k0);
           } else {
             const uint32_t full = b_full + 8 * stage;
             mbar_expect_tx(full, L::kStageBytes);
@@ -604,7 +537,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (t < 0) break;
         wait_ring(b_tempty + 8 * acc, aphase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * TN;
+        const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(b_full + 8 * stage, phase);
           tc_fence_after();
@@ -612,20 +545,14 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk) {
             const uint64_t ad = smem_desc<kTF32>(sA + kk * UK * SWZ, BOX_BYTES);
-#pragma unroll
-            for (int h = 0; h < kHalves; ++h) {   // wide: the second N = BN half of the tile
-              const uint64_t bd =
-                  smem_desc<kTF32>(sB + h * (kBH / CHUNK) * BOX_BYTES + kk * UK * SWZ, BOX_BYTES);
-              if (POS_SFB_EXP != 2 && POS_SFB_EXP != 3)
-                umma<kTF32, kPair>(d_tmem + h * BN, ad, bd, IDESC, (kb | kk) != 0);
-            }
+            const uint64_t bd = smem_desc<kTF32>(sB + kk * UK * SWZ, BOX_BYTES);
+            if (POS_SFB_EXP != 2 && POS_SFB_EXP != 3) umma<kTF32, kPair>(d_tmem, ad, bd, IDESC, (kb | kk) != 0);
           }
-          // frees the smem stage(s) when done (kMc: in all four CTAs — the V boxes are shared)
-          umma_commit<kPair>(b_empty + 8 * stage, kMc ? 0xF : 0x3);
+          umma_commit<kPair>(b_empty + 8 * stage);   // frees the smem stage(s) when done
           if (++stage == ST) { stage = 0; phase ^= 1; }
         }
-        umma_commit<kPair>(b_tfull + 8 * acc, (uint16_t)(0x3u << pbase));   // accumulator ready
-        if (++acc == NACC) { acc = 0; aphase ^= 1; }
+        umma_commit<kPair>(b_tfull + 8 * acc);        // accumulator ready for the epilogue(s)
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
       }
     }
   } else if (warp == 2) {
@@ -636,8 +563,8 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int it = 0;; ++it) {
         const int t = tile_of(it, rphase);
         if (t < 0) break;
-        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * TN;
-        const int nsub = nsub_of<TN>(ti.N, n0);
+        const int m0 = (t / ti.nb_n) * L::kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
+        const int nsub = nsub_of(ti.N, n0);
         for (int j = 0; j < nsub; ++j) {
           mbar_wait(b_wempty + 8 * ws, wphase ^ 1);
           const uint32_t wf = b_wfull + 8 * ws;
@@ -653,29 +580,6 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           if (++ws == WSLOTS) { ws = 0; wphase ^= 1; }
         }
       }
-    }
-  } else if (warp == 3) {
-    // ===================== W sub-tile storer (POS_SFB_STORER) =====================
-    if (POS_SFB_STORER && lane == 0) {
-      int ws = 0;
-      uint32_t uphase = 0, rphase = 0;
-      for (int it = 0;; ++it) {
-        const int t = tile_of(it, rphase);
-        if (t < 0) break;
-        const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * TN;
-        const int nsub = nsub_of<TN>(ti.N, n0);
-        for (int j = 0; j < nsub; ++j) {
-          mbar_wait(b_wupd + 8 * ws, uphase);       // the epilogue has updated the slot
-          if (POS_SFB_EXP != 1) {
-            tma_store_2d(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0);
-            bulk_commit();
-            bulk_wait_read<0>();                     // the store has read the slot
-          }
-          mbar_arrive(b_wempty + 8 * ws);            // the W producer may refill it
-          if (++ws == WSLOTS) { ws = 0; uphase ^= 1; }
-        }
-      }
-      bulk_wait_all();
     }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> regs, W += alpha * acc in smem, TMA store ========
@@ -693,15 +597,15 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (kPair) mbar_arrive_remote(map_rank(b_tempty + 8 * a, pbase));
+        if constexpr (kPair) mbar_arrive_remote(map_rank(b_tempty + 8 * a, 0));
         else mbar_arrive(b_tempty + 8 * a);
       }
     };
     for (int it = 0;; ++it) {
       const int t = tile_of(it, rphase);
       if (t < 0) break;
-      const int m0 = (t / ti.nb_n) * kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * TN;
-      const int nsub = nsub_of<TN>(ti.N, n0);
+      const int m0 = (t / ti.nb_n) * L::kTileRows + (int)crank * BM, n0 = (t % ti.nb_n) * BN;
+      const int nsub = nsub_of(ti.N, n0);
       // this group's sub-tiles of the tile: j = j0, j0 + EPI, ...; the last one frees TMEM
       const int j0 = (int)((g - (int)(sseq % EPI) + EPI) % EPI);
       const int jlast = j0 < nsub ? j0 + ((nsub - 1 - j0) / EPI) * EPI : -1;
@@ -709,11 +613,11 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       tc_fence_after();
       // A4b fused: the gathered v rows carry a 1.0 in column N, so accumulator column N of the
       // tile holding it is sum_j U[j][m] — the bias gradient of row m
-      if (g == 0 && ti.bias && (int64_t)n0 <= ti.N && ti.N < (int64_t)n0 + TN) {
+      if (g == 0 && ti.bias && (int64_t)n0 <= ti.N && ti.N < (int64_t)n0 + BN) {
         uint32_t bv;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
                      : "=r"(bv)
-                     : "r"(tmem_base + lane_addr + acc * TN + (uint32_t)(ti.N - n0)));
+                     : "r"(tmem_base + lane_addr + acc * BN + (uint32_t)(ti.N - n0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int64_t m = (int64_t)m0 + et;
         if (m < ti.M) {
@@ -727,12 +631,12 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const int ws = (int)(s % WSLOTS);
         const uint32_t wphase = (s / WSLOTS) & 1;
         uint32_t r[32];
-        tmem_ld32(tmem_base + lane_addr + acc * TN + j * WSUB, r);
+        tmem_ld32(tmem_base + lane_addr + acc * BN + j * WSUB, r);
         if (j == jlast) release_acc(acc);     // accumulator fully drained by this thread
         mbar_wait(b_wfull + 8 * ws, wphase);
         if (POS_SFB_EXP == 1) {   // diagnostic: no W traffic (TMEM drained, slot recycled)
           named_bar_sync(1 + g, 128);
-          if (et == 0) mbar_arrive((POS_SFB_STORER ? b_wupd : b_wempty) + 8 * ws);
+          if (et == 0) mbar_arrive(b_wempty + 8 * ws);
           continue;
         }
         const uint32_t row = sW0 + ws * W_BYTES + et * SWZ;
@@ -760,9 +664,7 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         fence_proxy_async_smem();             // generic-proxy smem writes -> visible to TMA
         named_bar_sync(1 + g, 128);
-        if (POS_SFB_STORER) {
-          if (et == 0) mbar_arrive(b_wupd + 8 * ws);   // the storer thread takes it from here
-        } else if (et == 0) {
+        if (et == 0) {
           if (POS_SFB_L2HINT)
             tma_store_2d_hint(&tmW, sW0 + ws * W_BYTES, n0 + j * WSUB, m0, policy_evict_first());
           else
@@ -781,9 +683,9 @@ sfb_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
       }
       sseq += (uint32_t)nsub;
-      if (++acc == NACC) { acc = 0; aphase ^= 1; }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
-    if (!POS_SFB_STORER && et == 0) bulk_wait_all();
+    if (et == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -838,36 +740,6 @@ bool encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint6
 #endif
 // CTA-pair kernel for K*P >= POS_SFB_PAIR_KP (env POS_SFB_PAIR=0|1 forces it off / on,
 // POS_SFB_PAIR_KP overrides the threshold; read at plan time).
-#ifndef POS_SFB_MC_KP
-#define POS_SFB_MC_KP (1LL << 40)   // off until measured (POS_SFB_MC=1 turns it on)
-#endif
-// 4-CTA multicast kernel (two pairs sharing the V boxes) for K*P >= POS_SFB_MC_KP among the pair
-// shapes (env POS_SFB_MC=0|1 forces it off / on; POS_SFB_MC_KP overrides the threshold).
-bool use_mc(int64_t KP) {
-  if (const char* f = getenv("POS_SFB_MC")) {
-    if (f[0] == '0') return false;
-    if (f[0] == '1') return true;
-  }
-  int64_t thr = POS_SFB_MC_KP;
-  if (const char* e = getenv("POS_SFB_MC_KP")) thr = atoll(e);
-  return KP >= thr;
-}
-
-#ifndef POS_SFB_WIDE_KP
-#define POS_SFB_WIDE_KP (1LL << 40)   // off until measured (POS_SFB_WIDE=1 turns it on)
-#endif
-// wide pair tile (256 x 512, one TMEM accumulator) for K*P >= POS_SFB_WIDE_KP among the pair
-// shapes (env POS_SFB_WIDE=0|1 forces it off / on; POS_SFB_WIDE_KP overrides the threshold)
-bool use_wide(int64_t KP) {
-  if (const char* f = getenv("POS_SFB_WIDE")) {
-    if (f[0] == '0') return false;
-    if (f[0] == '1') return true;
-  }
-  int64_t thr = POS_SFB_WIDE_KP;
-  if (const char* e = getenv("POS_SFB_WIDE_KP")) thr = atoll(e);
-  return KP >= thr;
-}
-
 // cluster_ok = false (the multi-GPU scheduler): no cluster launch unless POS_SFB_PAIR=1 forces it —
 // at P = 4 a CUDA-graph step with CTA-pair reconstructions next to the fused cross-GPU kernels
 // stalled a rank's factor pack until its peers' watchdogs fired (round 2)
@@ -882,49 +754,43 @@ bool use_pair(int64_t KP, bool cluster_ok) {
   return KP >= thr;
 }
 
-template <bool kTF32, bool kPair, bool kMc = false, bool kWide = false>
+template <bool kTF32, bool kPair>
 cudaError_t set_smem_attr() {
-  static cudaError_t e = cudaFuncSetAttribute(sfb_tc_kernel<kTF32, kPair, kMc, kWide>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              Lay<kPair, kWide>::kTotal);
+  static cudaError_t e = cudaFuncSetAttribute(
+      sfb_tc_kernel<kTF32, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<kPair>::kTotal);
   return e;
 }
 
-// Co-resident clusters of the pair kernel (kMc: of the 4-CTA multicast kernel) on this device
-// (0 = cannot launch as clusters)
-template <bool kTF32, bool kMc, bool kWide = false>
-int max_clusters() {
+// Co-resident CTA pairs of the pair kernel on this device (0 = cannot launch as clusters)
+template <bool kTF32>
+int max_pairs() {
   static int n = -1;
-  constexpr unsigned kCl = kMc ? 4 : 2;
   if (n < 0) {
     n = 0;
-    if (set_smem_attr<kTF32, true, kMc, kWide>() == cudaSuccess) {
+    if (set_smem_attr<kTF32, true>() == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(kCl * (unsigned)num_sms());
-      cfg.blockDim = dim3(Lay<true, kWide>::kThreads);
-      cfg.dynamicSmemBytes = Lay<true, kWide>::kTotal;
+      cfg.gridDim = dim3(2 * (unsigned)num_sms());
+      cfg.blockDim = dim3(Lay<true>::kThreads);
+      cfg.dynamicSmemBytes = Lay<true>::kTotal;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = kCl;
+      attr[0].val.clusterDim.x = 2;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int c = 0;
-      if (cudaOccupancyMaxActiveClusters(&c, sfb_tc_kernel<kTF32, true, kMc, kWide>, &cfg) ==
-          cudaSuccess)
+      if (cudaOccupancyMaxActiveClusters(&c, sfb_tc_kernel<kTF32, true>, &cfg) == cudaSuccess)
         n = c;
       else
         clear_stale_launch_error();
     }
     if (getenv("POS_SFB_VERBOSE"))
-      fprintf(stderr, "[poseidon] sfb_tc %s kernel: %d co-resident clusters of %u (%d SMs)\n",
-              kMc ? "multicast" : (kWide ? "wide pair" : "pair"), n, kCl, num_sms());
+      fprintf(stderr, "[poseidon] sfb_tc pair kernel: %d co-resident CTA pairs (%d SMs)\n", n,
+              num_sms());
   }
   return n;
 }
-template <bool kTF32>
-int max_pairs() { return max_clusters<kTF32, false>(); }
 
 template <bool kTF32>
 bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void* G, float* W,
@@ -959,38 +825,30 @@ bool make_plan_impl(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, const void*
     pl->tmB2 = pl->tmB;
   }
   pl->M = M; pl->N = N; pl->KP = KP;
-  int64_t TN = BN;   // tile columns (the wide pair tile: 2 BN), set once the variant is chosen
+  pl->nb_n = (int)((NB + BN - 1) / BN);
   pl->bias = bias;
   pl->nkb = (int)((KP + BK - 1) / BK);
   pl->tf32 = kTF32;
   int ctas = num_sms();
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
   pl->pair = use_pair(KP, cluster_ok) && ctas >= 2 && max_pairs<kTF32>() > 0;
-  pl->mc = pl->pair && use_mc(KP) && ctas >= 4 && max_clusters<kTF32, true>() > 0;
-  pl->wide = pl->pair && !pl->mc && use_wide(KP) && max_clusters<kTF32, false, true>() > 0;
-  if (pl->wide) TN = 2 * BN;
-  pl->nb_n = (int)((NB + TN - 1) / TN);
-  const int cl = pl->mc ? 4 : (pl->pair ? 2 : 1);   // CTAs per scheduling unit
-  const int64_t rows = (int64_t)cl * BM;
+  const int64_t rows = pl->pair ? 2 * BM : BM;
   const int64_t tiles = (int64_t)pl->nb_n * ((M + rows - 1) / rows);
   if (tiles > INT32_MAX) return false;
   pl->num_tiles = (int)tiles;
-  // persistent CTAs, or clusters — no more clusters than can be co-resident (a TPC with one
-  // usable SM cannot host a pair; a cluster that waits for a second wave would be a straggler)
-  int units = ctas;
-  if (pl->mc) units = std::min(ctas / 4, max_clusters<kTF32, true>());
-  else if (pl->wide) units = std::min(ctas / 2, max_clusters<kTF32, false, true>());
-  else if (pl->pair) units = std::min(ctas / 2, max_pairs<kTF32>());
+  // persistent CTAs, or CTA pairs — no more pairs than can be co-resident (a TPC with one
+  // usable SM cannot host a pair; a pair that waits for a second wave would be a straggler)
+  int units = pl->pair ? std::min(ctas / 2, max_pairs<kTF32>()) : ctas;
   if (units > pl->num_tiles) units = pl->num_tiles;
-  pl->grid = cl * units;
+  pl->grid = pl->pair ? 2 * units : units;
   return true;
 }
 
-template <bool kTF32, bool kPair, bool kMc = false, bool kWide = false>
+template <bool kTF32, bool kPair>
 cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
   clear_stale_launch_error();
-  constexpr int smem_bytes = Lay<kPair, kWide>::kTotal;
-  if (cudaError_t e = set_smem_attr<kTF32, kPair, kMc, kWide>(); e != cudaSuccess) return e;
+  constexpr int smem_bytes = Lay<kPair>::kTotal;
+  if (cudaError_t e = set_smem_attr<kTF32, kPair>(); e != cudaSuccess) return e;
   TileInfo ti;
   ti.M = pl.M; ti.N = pl.N; ti.KP = pl.KP;
   ti.nb_n = pl.nb_n; ti.num_tiles = pl.num_tiles; ti.nkb = pl.nkb;
@@ -1003,18 +861,18 @@ cudaError_t launch_plan_impl(const SfbTcPlan& pl, float alpha, int accumulate, c
   if constexpr (kPair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.grid);
-    cfg.blockDim = dim3(Lay<true, kWide>::kThreads);
+    cfg.blockDim = dim3(Lay<true>::kThreads);
     cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;   // the CTA pair shares one TPC
-    attr[0].val.clusterDim.x = kMc ? 4 : 2;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true, kMc, kWide>, pl.tmA, pl.tmB,
-                              pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
+    return cudaLaunchKernelEx(&cfg, sfb_tc_kernel<kTF32, true>, pl.tmA, pl.tmB, pl.tmW, pl.tmA2,
+                              pl.tmB2, ti, alpha, accumulate);
   } else {
     sfb_tc_kernel<kTF32, false><<<pl.grid, Lay<false>::kThreads, smem_bytes, s>>>(
         pl.tmA, pl.tmB, pl.tmW, pl.tmA2, pl.tmB2, ti, alpha, accumulate);
@@ -1044,12 +902,6 @@ bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t d
 }
 
 cudaError_t sfb_tc_launch(const SfbTcPlan& pl, float alpha, int accumulate, cudaStream_t s) {
-  if (pl.mc)
-    return pl.tf32 ? launch_plan_impl<true, true, true>(pl, alpha, accumulate, s)
-                   : launch_plan_impl<false, true, true>(pl, alpha, accumulate, s);
-  if (pl.wide)
-    return pl.tf32 ? launch_plan_impl<true, true, false, true>(pl, alpha, accumulate, s)
-                   : launch_plan_impl<false, true, false, true>(pl, alpha, accumulate, s);
   if (pl.pair)
     return pl.tf32 ? launch_plan_impl<true, true>(pl, alpha, accumulate, s)
                    : launch_plan_impl<false, true>(pl, alpha, accumulate, s);
