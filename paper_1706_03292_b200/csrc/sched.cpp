@@ -30,7 +30,7 @@
 
 namespace {
 
-constexpr int kPool = 6;    // apply streams: [0], [4] reconstructions; [1..3] dense applies;
+constexpr int kPool = 7;    // apply streams: [0], [4], [6] reconstructions; [1..3] dense applies;
                              // [5] flag-mode factor packs (high priority)
 constexpr int kTRing = 4;   // timing event sets per unit (iterations in flight)
 
@@ -103,7 +103,7 @@ struct pos_sched {
   bool captured = false;   // some iteration was issued under CUDA-graph stream capture
   int last_sfb = -1;       // most recently issued SFB unit of this iteration
   bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
-  int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1: one, in order)
+  int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1|2|3)
   // flag-mode packs on their own stream (POS_PACK_STREAM=1) instead of the comm stream: the PS
   // chain then starts with the first dense unit. Measured at P = 2 (round 2): VGG19 -7%, IncV3
   // -4%, but VGG19-22K +7% and AlexNet +17% (the packs gate the reconstructions there and slow
@@ -247,8 +247,9 @@ int issue_unit(pos_sched* s, int ui) {
   // Not with the CTA-pair (cluster) kernel: a cluster launch pending behind a running persistent
   // kernel on another stream can hold SMs that the cross-GPU kernels need (observed deadlock at
   // P = 4, AlexNet K*P = 512), so then all reconstructions stay on one stream.
-  const bool two = s->sfb_streams > 1 && !s->any_pair;
-  cudaStream_t as = un.scheme == POS_SCHEME_SFB ? s->pool[(two && (un.sfb_idx & 1)) ? 4 : 0]
+  static constexpr int kSfbPool[3] = {0, 4, 6};
+  const int nrs = s->any_pair ? 1 : s->sfb_streams;
+  cudaStream_t as = un.scheme == POS_SCHEME_SFB ? s->pool[kSfbPool[un.sfb_idx % nrs]]
                                                 : s->pool[1 + un.seq % 3];
   // first stage: the comm stream when a collective follows; else an auxiliary apply stream, so the
   // factor pack of the next SFB layer overlaps the reconstruction of this one
@@ -432,7 +433,7 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   s->L = n_layers;
   s->flags = flags;
   s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
-  if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = atoi(e) > 1 ? 2 : 1;
+  if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = std::max(1, std::min(3, atoi(e)));
   if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] == '1';
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
