@@ -57,6 +57,15 @@ inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4;
 
 int num_sms();
 
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first launch, and a load may have
+// to synchronise the context — fatal for kernels that spin on other GPUs' progress (the PS
+// barriers, the gather-flag wait): a rank blocked in a load while its own spinning kernel waits for
+// a peer that is blocked the same way only resolves through the watchdog. Every kernel of the
+// library is therefore loaded when a context is created (cudaFuncGetAttributes forces the load).
+cudaError_t preload_mem_kernels();
+cudaError_t preload_sfb_kernels();
+cudaError_t preload_symm_kernels();
+
 // Kernel launches report errors only through the runtime's last-error state, which other runtime
 // or NCCL calls may have left set (non-sticky, already reported to their callers). Clear it right
 // before launching so the check after the launch sees only the launch's own error; sticky device

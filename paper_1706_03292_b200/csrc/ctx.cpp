@@ -160,6 +160,17 @@ static int env_int(const char* name, int dflt) {
 
 static int ctx_common_init(pos_ctx* c) {
   POS_CUDA_TRY(cudaGetDevice(&c->device));
+  // load every kernel now (lazy loading could otherwise synchronise the context at a first launch
+  // while a spin-waiting kernel of this rank waits for a peer; see common.h)
+  {
+    static const cudaError_t preload = [] {
+      cudaError_t e = preload_mem_kernels();
+      if (e == cudaSuccess) e = preload_sfb_kernels();
+      if (e == cudaSuccess) e = preload_symm_kernels();
+      return e;
+    }();
+    POS_CUDA_TRY(preload);
+  }
   int lo = 0, hi = 0;
   POS_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   // comm stream priority: the greatest by default; POS_COMM_PRIO=n sets lo + n (clamped), an

@@ -246,4 +246,18 @@ cudaError_t ktrace_reset(unsigned long long* rec) {
   return e != cudaSuccess ? e : cudaDeviceSynchronize();
 }
 
+cudaError_t preload_mem_kernels() {
+  using bf = __nv_bfloat16;
+  cudaFuncAttributes fa;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(pack_kernel<bf, true>), reinterpret_cast<const void*>(pack_kernel<float, true>),
+      reinterpret_cast<const void*>(pack_kernel<bf, false>), reinterpret_cast<const void*>(pack_kernel<float, false>),
+      reinterpret_cast<const void*>(bias_colsum_kernel<bf>), reinterpret_cast<const void*>(bias_colsum_kernel<float>),
+      reinterpret_cast<const void*>(ps_apply_vec_kernel), reinterpret_cast<const void*>(ps_apply_scalar_kernel),
+      reinterpret_cast<const void*>(sim_ps_reduce_apply_kernel), reinterpret_cast<const void*>(ktrace_init_kernel)};
+  for (const void* f : fns)
+    if (cudaError_t e = cudaFuncGetAttributes(&fa, f); e != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
 }  // namespace pos

@@ -93,4 +93,11 @@ cudaError_t launch_sfb_simt(int64_t M, int64_t N, int64_t KP, int32_t dtype, con
   return cudaGetLastError();
 }
 
+
+cudaError_t preload_simt_kernels() {
+  cudaFuncAttributes fa;
+  if (cudaError_t e = cudaFuncGetAttributes(&fa, sfb_simt_kernel<__nv_bfloat16>); e != cudaSuccess) return e;
+  return cudaFuncGetAttributes(&fa, sfb_simt_kernel<float>);
+}
+
 }  // namespace pos

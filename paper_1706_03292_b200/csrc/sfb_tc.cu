@@ -917,4 +917,23 @@ cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const
   return sfb_tc_launch(pl, alpha, accumulate, s);
 }
 
+
+cudaError_t preload_simt_kernels();   // sfb_simt.cu
+
+cudaError_t preload_sfb_kernels() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {reinterpret_cast<const void*>(sfb_tc_kernel<false, false>),
+                       reinterpret_cast<const void*>(sfb_tc_kernel<true, false>),
+                       reinterpret_cast<const void*>(sfb_tc_kernel<false, true>),
+                       reinterpret_cast<const void*>(sfb_tc_kernel<true, true>)};
+  for (const void* f : fns)
+    if (cudaError_t e = cudaFuncGetAttributes(&fa, f); e != cudaSuccess) return e;
+  // the launch attributes and the co-residency queries the plans use, off the hot path too
+  if (cudaError_t e = set_smem_attr<false, false>(); e != cudaSuccess) return e;
+  if (cudaError_t e = set_smem_attr<true, false>(); e != cudaSuccess) return e;
+  (void)max_pairs<false>();
+  (void)max_pairs<true>();
+  return preload_simt_kernels();
+}
+
 }  // namespace pos

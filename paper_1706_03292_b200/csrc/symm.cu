@@ -694,6 +694,29 @@ int symm_wait_gathered(pos_ctx* c, const uint32_t* flags, const unsigned* fstate
   return POS_OK;
 }
 
+
+cudaError_t preload_symm_kernels() {
+  using bf = __nv_bfloat16;
+  cudaFuncAttributes fa;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(ps_sync_kernel<true, true>),
+      reinterpret_cast<const void*>(ps_sync_kernel<false, true>),
+      reinterpret_cast<const void*>(ps_sync_kernel<false, false>),
+#define POS_PK(T, B, F, M) reinterpret_cast<const void*>(pack_x_kernel<T, B, F, M>)
+      POS_PK(bf, true, true, true), POS_PK(bf, true, true, false), POS_PK(bf, true, false, true),
+      POS_PK(bf, true, false, false), POS_PK(bf, false, true, true), POS_PK(bf, false, true, false),
+      POS_PK(bf, false, false, true), POS_PK(bf, false, false, false), POS_PK(float, true, true, true),
+      POS_PK(float, true, true, false), POS_PK(float, true, false, true), POS_PK(float, true, false, false),
+      POS_PK(float, false, true, true), POS_PK(float, false, true, false), POS_PK(float, false, false, true),
+      POS_PK(float, false, false, false),
+#undef POS_PK
+      reinterpret_cast<const void*>(wait_flags_kernel),
+      reinterpret_cast<const void*>(resolve_window_kernel)};
+  for (const void* f : fns)
+    if (cudaError_t e = cudaFuncGetAttributes(&fa, f); e != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
 }  // namespace pos
 
 using namespace pos;
