@@ -39,7 +39,7 @@ def digest(t):
 PS_SIZES = [1, 10, 63, 4097, 16400, 38720, 590080, 2359808]
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("P", [2, 3, 4, 8, 16])
 @pytest.mark.parametrize("n", PS_SIZES)
 def test_loop_ps_exact_bitwise_all_replicas(P, n):
     """Shard tails, empty shards (n < 64 P), the n = 16400 grid case of ADVICE r1; 3 iterations."""
@@ -119,7 +119,7 @@ def loop_fc_run(P, K, M, N, dtype, in_dtype, regime, iters=3, seed=0, bias=True)
     return W0, Wd, bd, Wr, br
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
 @pytest.mark.parametrize("dtype,in_dtype", [("bf16", "bf16"), ("tf32", "f32"), ("f32", "f32")])
 @pytest.mark.parametrize("MN", [(64, 64), (65, 132), (1000, 4100), (257, 1028)])
 def test_loop_fc_exact_bitwise_3iter(P, dtype, in_dtype, MN):
