@@ -112,6 +112,8 @@ def parse():
     a = ap.parse_args()
     if a.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if a.dtype == "f32":
+        a.no_trace = True    # the exact-fp32 SIMT reconstruction is not traced: CUDA-event timing
     return a
 
 
@@ -785,17 +787,22 @@ def run_ours(a):
             traffic = tj[key].get("a4_dram_bytes_per_step")
     achieved = a4_bytes / (a4_ms / 1e3) / 1e9 if a4_ms > 0 else None
     span_achieved = a4_bytes / (a4_span_ms / 1e3) / 1e9 if a4_span_ms else None
-    roof = {"kernel": "sfb_tc_kernel (A4 reconstruct-and-apply, all SFB layers of one step)",
+    roof = {"kernel": ("sfb_simt_kernel (A4 exact-fp32 reconstruct-and-apply, FFMA" if a.dtype == "f32" else
+                       "sfb_tc_kernel (A4 reconstruct-and-apply") + ", all SFB layers of one step)",
             "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic,
             "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
             "launches_per_step": n_a4, "avg_launch_ms": a4_ms / n_a4 if n_a4 else None,
-            "kernel_ms_note": "per-launch durations from the device-side trace (%globaltimer stamped by "
-                              "the kernels: first CTA start to last CTA end; no events in the captured "
-                              "step) of a replay of the same step right after the (untraced) timed "
-                              "region, as many steps, averaged and summed over the step's launches; "
-                              "achieved = algorithmic bytes of those launches / that sum",
+            "kernel_ms_note": ("per-launch durations from CUDA events around each apply stage inside the "
+                               "timed step graphs (--no-trace), averaged and summed over the step's "
+                               "launches; achieved = algorithmic bytes of those launches / that sum")
+                              if a.no_trace else
+                              ("per-launch durations from the device-side trace (%globaltimer stamped by "
+                               "the kernels: first CTA start to last CTA end; no events in the captured "
+                               "step) of a replay of the same step right after the (untraced) timed "
+                               "region, as many steps, averaged and summed over the step's launches; "
+                               "achieved = algorithmic bytes of those launches / that sum"),
             "span_ms": a4_span_ms, "span_achieved": span_achieved,
             "span_frac": span_achieved / peaks["hbm_gbs"] if span_achieved else None,
             "span_note": "first reconstruction CTA start to last one's end in a step (consecutive layers' "
