@@ -3,9 +3,7 @@
 // tcgen05 has no fp32-input kind (reading S16), so the "pure fp32" mode is a shared-memory tiled
 // FFMA GEMM with fp32 accumulation in a fixed k order. Also used for BF16/TF32 factors when the
 // caller's W cannot be addressed by TMA (ldw % 4 != 0 or W not 16-byte aligned).
-// Tile 128 x 128, BK 16, 256 threads, 8 x 8 outputs per thread: rows ty + 16 i, columns
-// 4 tx + {0..3} and 64 + 4 tx + {0..3}, so the W read-modify-write (the HBM-dominant traffic) moves
-// 16-byte vectors when the row is 16-byte aligned (ldw % 4 == 0, W aligned).
+// Tile 128 x 128, BK 16, 256 threads, 8 x 8 outputs per thread.
 #include <cuda_bf16.h>
 
 #include "common.h"
@@ -22,8 +20,8 @@ template <typename T>
 __global__ void __launch_bounds__(THREADS)
 sfb_simt_kernel(const T* __restrict__ U, const T* __restrict__ V, int64_t R, int64_t M, int64_t N,
                 int64_t KP, int accumulate, float* __restrict__ W, int64_t ldw, float alpha) {
-  __shared__ __align__(16) float As[TK][TM + 4];
-  __shared__ __align__(16) float Bs[TK][TN + 4];
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
   const int64_t m0 = (int64_t)blockIdx.y * TM, n0 = (int64_t)blockIdx.x * TN;
@@ -50,10 +48,8 @@ sfb_simt_kernel(const T* __restrict__ U, const T* __restrict__ V, int64_t R, int
       float a[8], b[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) a[i] = As[kk][ty + 16 * i];
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][4 * tx]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[kk][64 + 4 * tx]);
-      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -61,29 +57,17 @@ sfb_simt_kernel(const T* __restrict__ U, const T* __restrict__ V, int64_t R, int
     }
     __syncthreads();
   }
-  const bool vec = ((reinterpret_cast<uintptr_t>(W) & 15u) == 0) && (ldw % 4) == 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t m = m0 + ty + 16 * i;
     if (m >= M) continue;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t n = n0 + 64 * h + 4 * tx;
-      float* p = W + m * ldw + n;
-      if (vec && n + 3 < N) {
-        float4 w = accumulate ? *reinterpret_cast<const float4*>(p) : make_float4(0.f, 0.f, 0.f, 0.f);
-        w.x = fmaf(alpha, acc[i][4 * h + 0], w.x);
-        w.y = fmaf(alpha, acc[i][4 * h + 1], w.y);
-        w.z = fmaf(alpha, acc[i][4 * h + 2], w.z);
-        w.w = fmaf(alpha, acc[i][4 * h + 3], w.w);
-        *reinterpret_cast<float4*>(p) = w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (n + q < N) {
-            const float base = accumulate ? p[q] : 0.0f;
-            p[q] = fmaf(alpha, acc[i][4 * h + q], base);
-          }
+    for (int j = 0; j < 8; ++j) {
+      const int64_t n = n0 + tx + 16 * j;
+      if (n < N) {
+        float* p = W + m * ldw + n;
+        const float base = accumulate ? *p : 0.0f;
+        *p = fmaf(alpha, acc[i][j], base);
       }
     }
   }
