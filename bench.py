@@ -112,8 +112,6 @@ def parse():
     a = ap.parse_args()
     if a.warmup < 3:
         ap.error("--warmup must be >= 3")
-    if a.dtype == "f32":
-        a.no_trace = True    # the exact-fp32 SIMT reconstruction is not traced: CUDA-event timing
     return a
 
 
@@ -323,7 +321,7 @@ def isolated_kernels(pos, model, units, K, P, dtype, peaks):
         ly = max(fcs, key=lambda l: l.M * l.N)
         M, N, KP = ly.M, ly.N, K * P
         R = pos.pos_factor_row_elems(M, N)
-        G = (torch.randn(KP, R, device=dev) * 0.03).to(fdt)
+        G = (torch.randn(pos.pos_factor_slot_rows(KP, dt), R, device=dev) * 0.03).to(fdt)
         Ws = [torch.randn(M, N, device=dev) for _ in range(2)]
         b = torch.zeros(M, device=dev)
         ms = timed(lambda i: pos.pos_reconstruct_apply(M, N, KP, dt, G, Ws[i], b, -1e-3))
@@ -334,7 +332,7 @@ def isolated_kernels(pos, model, units, K, P, dtype, peaks):
             "frac_bf16_peak": 2 * M * N * KP / ms / 1e9 / peaks["bf16_tflops"]}
         u = torch.randn(K, M, device=dev).to(fdt)
         v = torch.randn(K, N, device=dev).to(fdt)
-        slots = [torch.empty(K * R, device=dev, dtype=fdt) for _ in range(2)]
+        slots = [torch.empty(pos.pos_factor_slot_rows(K, dt) * R, device=dev, dtype=fdt) for _ in range(2)]
         ms = timed(lambda i: pos.pos_pack_factors(u, v, slots[i], dt), n_launch=50)
         byts = K * (M + N) * (eb + eb)
         out["a2_pack"] = {"layer": f"{ly.name} K={K}", "us": ms * 1e3, "achieved_gbs": byts / ms / 1e6,
@@ -787,8 +785,9 @@ def run_ours(a):
             traffic = tj[key].get("a4_dram_bytes_per_step")
     achieved = a4_bytes / (a4_ms / 1e3) / 1e9 if a4_ms > 0 else None
     span_achieved = a4_bytes / (a4_span_ms / 1e3) / 1e9 if a4_span_ms else None
-    roof = {"kernel": ("sfb_simt_kernel (A4 exact-fp32 reconstruct-and-apply, FFMA" if a.dtype == "f32" else
-                       "sfb_tc_kernel (A4 reconstruct-and-apply") + ", all SFB layers of one step)",
+    roof = {"kernel": ("sfb_tc_kernel (A4 reconstruct-and-apply, fp32 as 3xTF32: 3 tf32 rows per pair"
+                       if a.dtype == "f32" else "sfb_tc_kernel (A4 reconstruct-and-apply")
+                      + ", all SFB layers of one step)",
             "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
             "traffic": traffic,

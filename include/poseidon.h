@@ -141,6 +141,12 @@ int64_t pos_padded_size(int64_t n, int32_t P);
  * of the v part is the "ones column" that makes the reconstruction GEMM also produce the bias
  * gradient sum_j u_j, reading S12). */
 int64_t pos_factor_row_elems(int64_t M, int64_t N);
+/* Gathered rows that K factor pairs occupy in dtype: K for BF16 / TF32, 3K for F32, which runs as
+ * 3xTF32 on the tensor cores (reading S16): the pair k is packed as rows k, K+k, 2K+k holding
+ * (tf32(u), tf32(v)), (tf32(u), lo(v)), (lo(u), tf32(v)) with lo(x) = tf32(x - tf32(x)); tf32() rounds
+ * to nearest, ties away. The contraction over the three rows is u^T v up to the lo(u) lo(v) term and
+ * the rounding of lo (relative error ~2^-21 per product). Negative on bad arguments. */
+int64_t pos_factor_slot_rows(int64_t K, int32_t dtype);
 
 /* ======================================================================================
  * Context: owns the NCCL communicator, a comm stream, a stream pool and scratch buffers.
@@ -199,19 +205,22 @@ int pos_set_max_ctas(pos_ctx* ctx, int32_t max_ctas);
 /* A2 — SFB factor pack ("transformation between SFs and gradients"): write the K rows
  *   slot[k][0 .. M_pad)            = dtype(u[k][0..M)), zero in [M, M_pad)
  *   slot[k][M_pad .. M_pad+N_pad)  = dtype(v[k][0..N)), 1.0 at M_pad+N (ones column), zero after
- * slot: device, K * pos_factor_row_elems(M,N) elements of bf16 (dtype BF16) or fp32 (TF32/F32),
- * 16-byte aligned. u, v: device, in_dtype storage, any alignment. */
+ * (F32: the 3K rows of pos_factor_slot_rows, each value split as stated there; the ones column
+ * splits into 1 / 0 / 1 across the three blocks.)
+ * slot: device, pos_factor_slot_rows(K, dtype) * pos_factor_row_elems(M,N) elements of bf16 (dtype
+ * BF16) or fp32 (TF32/F32), 16-byte aligned. u, v: device, in_dtype storage, any alignment. */
 int pos_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                      const void* u, const void* v, void* slot, void* stream);
 
 /* A4 + A4b — SFB reconstruct-and-apply (Eq. 2):
  *   W[m][n] = (accumulate ? W[m][n] : 0) + alpha * sum_{j < KP} U[j][m] * V[j][n]
  *   b[m]    = (accumulate ? b[m]    : 0) + alpha * sum_{j < KP} U[j][m]        (if b != NULL)
- * where row j of the gathered buffer G (KP rows of pos_factor_row_elems(M,N) elements, packed by
- * pos_pack_factors, worker-major: j = p*K + k) holds [u_j | v_j]. W: device fp32, row stride ldw
- * elements (ldw >= N). BF16/TF32 run the tcgen05/TMEM/TMA kernel when N % 4 == 0, ldw % 4 == 0 and W is
- * 16-byte aligned (else the SIMT kernel); F32 always runs the exact SIMT FFMA kernel. The k order
- * is fixed, so results are bitwise reproducible. */
+ * where row j of the gathered buffer G (pos_factor_slot_rows(KP, dtype) rows of
+ * pos_factor_row_elems(M,N) elements, packed by pos_pack_factors, worker-major: slot p of K pairs
+ * first) holds [u_j | v_j] (F32: the three 3xTF32 rows of each pair, summed). W: device fp32, row
+ * stride ldw elements (ldw >= N). Every dtype runs the tcgen05/TMEM/TMA kernel (F32 with the tf32
+ * kind over 3*KP rows) when N % 4 == 0, ldw % 4 == 0 and W is 16-byte aligned, else the SIMT FFMA
+ * kernel. The k order is fixed, so results are bitwise reproducible. */
 int pos_reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                           int32_t accumulate, float* W, int64_t ldw, float* b, float alpha,
                           void* stream);

@@ -100,6 +100,10 @@ def pos_factor_row_elems(M: int, N: int) -> int:
     return _chk(lib().pos_factor_row_elems(M, N), "pos_factor_row_elems")
 
 
+def pos_factor_slot_rows(K: int, dtype: int) -> int:
+    return _chk(lib().pos_factor_slot_rows(K, dtype), "pos_factor_slot_rows")
+
+
 # --------------------------------------------------------------------- torch marshalling ----
 def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())

@@ -27,6 +27,7 @@ SIGNATURES = {
     "pos_scheme_time_adam_b200": (C.c_int, [i64, i64, i64, i32, i32, f64, f64, f64, P_f64]),
     "pos_padded_size": (i64, [i64, i32]),
     "pos_factor_row_elems": (i64, [i64, i64]),
+    "pos_factor_slot_rows": (i64, [i64, i32]),
     "pos_get_unique_id": (C.c_int, [vp]),
     "pos_init": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
     "pos_init_local": (C.c_int, [i32, C.POINTER(vp)]),

@@ -54,6 +54,11 @@ inline int64_t m_pad(int64_t M) { return round_up(M, 64); }
 inline int64_t n_pad(int64_t N) { return round_up(N + 1, 64); }
 inline int64_t row_elems(int64_t M, int64_t N) { return m_pad(M) + n_pad(N); }
 inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4; }
+// Gathered rows per sufficient-factor pair. POS_DT_F32 runs as 3xTF32 on the tensor cores
+// (reading S16): the pack writes each pair three times, as K-row blocks (hi u, hi v),
+// (hi u, lo v), (lo u, hi v) with hi = tf32(x), lo = tf32(x - hi), so one tf32 contraction over
+// 3K rows per slot gives sum_k hi·hi + hi·lo + lo·hi = u_k^T v_k up to the dropped lo·lo term.
+inline int64_t rows_per_sample(int32_t dtype) { return dtype == POS_DT_F32 ? 3 : 1; }
 
 int num_sms();
 
@@ -188,11 +193,36 @@ __device__ __forceinline__ uint4 pack_chunk(const Tin* __restrict__ src, int64_t
   }
   return o;
 }
+
+// 3xTF32 split (POS_DT_F32): part 1 = tf32 head (round to nearest, ties away), part 2 = the fp32
+// remainder x - head, itself rounded to tf32 (the tensor core reads only tf32 bits). 1.0 (the ones
+// column) splits into 1 + 0 and 0 into 0 + 0, so the ones column is 1 in blocks 0 and 2 and 0 in
+// block 1: the fused bias column sums hi u + lo u = u.
+__device__ __forceinline__ float tf32_part(float x, int part) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  if (part == 1) return __uint_as_float(h);
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - __uint_as_float(h)));
+  return __uint_as_float(l);
+}
+__device__ __forceinline__ uint4 tf32_split4(uint4 q, int part) {
+  return make_uint4(__float_as_uint(tf32_part(__uint_as_float(q.x), part)),
+                    __float_as_uint(tf32_part(__uint_as_float(q.y), part)),
+                    __float_as_uint(tf32_part(__uint_as_float(q.z), part)),
+                    __float_as_uint(tf32_part(__uint_as_float(q.w), part)));
+}
+// gathered row r of a 3xTF32 slot of K pairs: pair r % K, block r / K; the u part is lo in
+// block 2, the v part lo in block 1, hi otherwise
+__device__ __forceinline__ int split_part(int64_t block, bool v_part) {
+  return (v_part ? block == 1 : block == 2) ? 2 : 1;
+}
 #endif
 
 // ---- kernel launchers (return cudaError_t of the launch) ----
 cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
                                 const void* u, const void* v, void* slot, cudaStream_t s);
+// b += alpha * sum_j U[j][m] * V[j][N] over KP gathered ROWS (V[j][N] = the ones column's value)
 cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                                int32_t accumulate, float* b, float alpha, cudaStream_t s);
 // tr.rec != nullptr: traced; tr.expected = 0 means "this launch alone" (set to its grid)
@@ -216,11 +246,13 @@ inline bool gather_flag_mode(int32_t dtype, int64_t N) {
 }
 cudaError_t launch_sim_ps_reduce_apply(const float* const* grads, int P, float* W, int64_t n,
                                        float alpha, cudaStream_t s);
-// SIMT fp32 FFMA reconstruct-and-apply (POS_DT_F32, and the odd-ldw path)
+// SIMT fp32 FFMA reconstruct-and-apply (shapes the TMA path cannot take: N or ldw % 4 != 0,
+// unaligned W). KP here = gathered ROWS (samples * rows_per_sample).
 cudaError_t launch_sfb_simt(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                             int32_t accumulate, float* W, int64_t ldw, float alpha,
                             cudaStream_t s);
-// tcgen05 / TMEM / TMA reconstruct-and-apply (POS_DT_BF16 / POS_DT_TF32). Returns
+// tcgen05 / TMEM / TMA reconstruct-and-apply (all dtypes; POS_DT_F32 = tf32 kind over the 3xTF32
+// rows). KP = SAMPLES (K * P) here and in the plan / pair queries below. Returns
 // cudaErrorNotSupported if the shape/alignment cannot use TMA (caller falls back to SIMT).
 // b != nullptr: the bias update is fused (needs the ones column of the packed v rows).
 cudaError_t launch_sfb_tc(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,

@@ -317,7 +317,7 @@ int pos_sync_layer_sfb(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_d
   if ((rc = ctx_check(c))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const int P = c->world;
-  const int64_t R = row_elems(M, N), slot = K * R;
+  const int64_t R = row_elems(M, N), slot = K * rows_per_sample(dtype) * R;
   void* G = nullptr;
   if ((rc = ctx_workspace(c, (size_t)(slot * P * dtype_bytes(dtype)), &G))) return rc;
   uint8_t* my_slot = static_cast<uint8_t*>(G) + (size_t)(c->rank * slot * dtype_bytes(dtype));
@@ -361,7 +361,9 @@ int pos_sync_layer_fc_ps(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in
   if ((rc = ctx_check(c))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   void* buf = nullptr;
-  if ((rc = ctx_workspace(c, (size_t)(K * row_elems(M, N) * dtype_bytes(dtype)), &buf))) return rc;
+  if ((rc = ctx_workspace(c, (size_t)(K * rows_per_sample(dtype) * row_elems(M, N) * dtype_bytes(dtype)),
+                         &buf)))
+    return rc;
   if ((rc = stage_fc_local_grad(c, M, N, K, in_dtype, dtype, u, v, buf, grad, has_bias, s)))
     return rc;
   return stage_ps_dense(c, M * N + (has_bias ? M : 0), grad, Wb, alpha, s, nullptr, nullptr,
@@ -379,7 +381,7 @@ int pos_sim_sync_layer_sfb(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t 
   POS_CHECK_ARG(u && v && W, "NULL pointer");
   cudaStream_t s = (cudaStream_t)stream;
   const int P = c->world;
-  const int64_t slot = K * row_elems(M, N);
+  const int64_t slot = K * rows_per_sample(dtype) * row_elems(M, N);
   void* G = nullptr;
   if ((rc = ctx_workspace(c, (size_t)(slot * P * dtype_bytes(dtype)), &G))) return rc;
   for (int p = 0; p < P; ++p) {

@@ -181,6 +181,14 @@ int64_t pos_factor_row_elems(int64_t M, int64_t N) {
   return row_elems(M, N);
 }
 
+int64_t pos_factor_slot_rows(int64_t K, int32_t dtype) {
+  clear_error();
+  POS_CHECK_ARG(K >= 0, "K must be >= 0");
+  POS_CHECK_ARG(dtype == POS_DT_BF16 || dtype == POS_DT_TF32 || dtype == POS_DT_F32,
+                "bad dtype %d", dtype);
+  return K * rows_per_sample(dtype);
+}
+
 // ---- kernel building blocks ----
 
 int pos_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtype, int32_t dtype,
@@ -228,16 +236,17 @@ int reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const voi
   POS_CHECK_ARG(aligned16(G), "G must be 16-byte aligned");
   POS_CHECK_ARG((M * ldw) / ldw == M, "M * ldw overflows");
   cudaError_t e;
-  const bool tc = dtype != POS_DT_F32 && sfb_tc_supported(N, ldw, W, G);
+  const bool tc = sfb_tc_supported(N, ldw, W, G);
+  const int64_t rows = KP * rows_per_sample(dtype);   // 3xTF32 rows for POS_DT_F32
   if (tc) {   // bias fused into the tensor-core epilogue (ones column)
     e = launch_sfb_tc(M, N, KP, dtype, G, accumulate, W, ldw, b, alpha, max_ctas, s);
   } else {
-    e = launch_sfb_simt(M, N, KP, dtype, G, accumulate, W, ldw, alpha, s);
+    e = launch_sfb_simt(M, N, rows, dtype, G, accumulate, W, ldw, alpha, s);
   }
   if (e != cudaSuccess)
     POS_FAIL(POS_ECUDA, "reconstruct kernel launch failed: %s", cudaGetErrorString(e));
   if (b && !tc) {
-    e = launch_bias_colsum(M, N, KP, dtype, G, accumulate, b, alpha, s);
+    e = launch_bias_colsum(M, N, rows, dtype, G, accumulate, b, alpha, s);
     if (e != cudaSuccess)
       POS_FAIL(POS_ECUDA, "bias kernel launch failed: %s", cudaGetErrorString(e));
   }

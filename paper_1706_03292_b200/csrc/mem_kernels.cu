@@ -24,9 +24,10 @@ __device__ __forceinline__ float ld_in(const float* p) { return *p; }
 template <typename Tin, bool kBF16>
 __global__ void pack_kernel(const Tin* __restrict__ u, const Tin* __restrict__ v,
                             void* __restrict__ out, int64_t M, int64_t N, int64_t Mp, int64_t R,
-                            int64_t k0) {
+                            int64_t r0, int64_t K, int split) {
   constexpr int VEC = kBF16 ? 8 : 4;
-  const int64_t k = k0 + blockIdx.y;
+  const int64_t r = r0 + blockIdx.y;                                  // gathered row
+  const int64_t k = split ? r % K : r;                                // its factor pair
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // VEC-element chunk in row
   const int64_t col = c * VEC;
   if (col >= R) return;
@@ -38,18 +39,23 @@ __global__ void pack_kernel(const Tin* __restrict__ u, const Tin* __restrict__ v
   // sum_j u_j, the bias gradient (A4b fused into A4); every other pad element is 0
   const int64_t onec = col < Mp ? -1 : N;
   const int64_t eb = kBF16 ? 2 : 4;
-  *reinterpret_cast<uint4*>(static_cast<char*>(out) + (k * R + col) * eb) =
-      pack_chunk<Tin, kBF16>(src, idx, lim, onec);
+  uint4 q = pack_chunk<Tin, kBF16>(src, idx, lim, onec);
+  if constexpr (!kBF16)
+    if (split) q = tf32_split4(q, split_part(r / K, col >= Mp));
+  *reinterpret_cast<uint4*>(static_cast<char*>(out) + (r * R + col) * eb) = q;
 }
 
 // ---------------------------------------------------------------------------------------------
 // A4b: block = 32 columns x 8 warps. Warp w sums the contiguous row range [w*chunk, (w+1)*chunk)
 // for its lane's column; the 8 partials are then added in warp order. Fixed order => bitwise
-// reproducible; every rank computes the same value from the same gathered U.
+// reproducible; every rank computes the same value from the same gathered U. Each row is weighted
+// by its ones-column entry (column onec = M_pad + N): 1 everywhere except the (hi u, lo v) block
+// of a 3xTF32 slot, where it is 0 — the same sum the tensor-core path takes from column N.
 // ---------------------------------------------------------------------------------------------
 template <typename T>
 __global__ void bias_colsum_kernel(const T* __restrict__ G, int64_t M, int64_t R, int64_t KP,
-                                   int accumulate, float* __restrict__ b, float alpha) {
+                                   int64_t onec, int accumulate, float* __restrict__ b,
+                                   float alpha) {
   __shared__ float part[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t m = (int64_t)blockIdx.x * 32 + lane;
@@ -57,7 +63,7 @@ __global__ void bias_colsum_kernel(const T* __restrict__ G, int64_t M, int64_t R
   const int64_t j0 = w * chunk, j1 = min(KP, j0 + chunk);
   float s = 0.0f;
   if (m < M)
-    for (int64_t j = j0; j < j1; ++j) s += ld_in(G + j * R + m);
+    for (int64_t j = j0; j < j1; ++j) s = fmaf(ld_in(G + j * R + m), ld_in(G + j * R + onec), s);
   part[w][lane] = s;
   __syncthreads();
   if (w == 0 && m < M) {
@@ -164,17 +170,19 @@ cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtyp
   const int threads = 128;
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
   const int64_t chunks = R / vec;
-  for (int64_t k0 = 0; k0 < K; k0 += 65535) {
-    const unsigned rows = (unsigned)std::min<int64_t>(65535, K - k0);
-    dim3 grid((unsigned)((chunks + threads - 1) / threads), rows);
+  const int64_t rows = K * rows_per_sample(dtype);
+  const int split = dtype == POS_DT_F32;
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const unsigned nr = (unsigned)std::min<int64_t>(65535, rows - r0);
+    dim3 grid((unsigned)((chunks + threads - 1) / threads), nr);
     using bf = __nv_bfloat16;
     const bool in_bf = in_dtype == POS_IN_BF16;
     if (dtype == POS_DT_BF16) {
-      if (in_bf) pack_kernel<bf, true><<<grid, threads, 0, s>>>(static_cast<const bf*>(u), static_cast<const bf*>(v), slot, M, N, Mp, R, k0);
-      else       pack_kernel<float, true><<<grid, threads, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(v), slot, M, N, Mp, R, k0);
+      if (in_bf) pack_kernel<bf, true><<<grid, threads, 0, s>>>(static_cast<const bf*>(u), static_cast<const bf*>(v), slot, M, N, Mp, R, r0, K, 0);
+      else       pack_kernel<float, true><<<grid, threads, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(v), slot, M, N, Mp, R, r0, K, 0);
     } else {
-      if (in_bf) pack_kernel<bf, false><<<grid, threads, 0, s>>>(static_cast<const bf*>(u), static_cast<const bf*>(v), slot, M, N, Mp, R, k0);
-      else       pack_kernel<float, false><<<grid, threads, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(v), slot, M, N, Mp, R, k0);
+      if (in_bf) pack_kernel<bf, false><<<grid, threads, 0, s>>>(static_cast<const bf*>(u), static_cast<const bf*>(v), slot, M, N, Mp, R, r0, K, split);
+      else       pack_kernel<float, false><<<grid, threads, 0, s>>>(static_cast<const float*>(u), static_cast<const float*>(v), slot, M, N, Mp, R, r0, K, split);
     }
   }
   return cudaGetLastError();
@@ -183,14 +191,14 @@ cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtyp
 cudaError_t launch_bias_colsum(int64_t M, int64_t N, int64_t KP, int32_t dtype, const void* G,
                                int32_t accumulate, float* b, float alpha, cudaStream_t s) {
   clear_stale_launch_error();
-  const int64_t R = row_elems(M, N);
+  const int64_t R = row_elems(M, N), onec = m_pad(M) + N;
   const unsigned blocks = (unsigned)((M + 31) / 32);
   if (dtype == POS_DT_BF16)
-    bias_colsum_kernel<<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(G), M, R, KP,
+    bias_colsum_kernel<<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(G), M, R, KP, onec,
                                               accumulate, b, alpha);
   else
-    bias_colsum_kernel<<<blocks, 256, 0, s>>>(static_cast<const float*>(G), M, R, KP, accumulate,
-                                              b, alpha);
+    bias_colsum_kernel<<<blocks, 256, 0, s>>>(static_cast<const float*>(G), M, R, KP, onec,
+                                              accumulate, b, alpha);
   return cudaGetLastError();
 }
 

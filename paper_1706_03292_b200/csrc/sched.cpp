@@ -282,7 +282,7 @@ int issue_unit(pos_sched* s, int ui) {
   }
   if (ts && (rc = trec(ts->start, cs))) return rc;
   if (un.scheme == POS_SCHEME_SFB) {
-    const int64_t R = row_elems(un.M, un.N), slot = un.K * R;
+    const int64_t R = row_elems(un.M, un.N), slot = un.K * rows_per_sample(un.dtype) * R;
     uint8_t* my_slot =
         static_cast<uint8_t*>(un.gbuf) + (size_t)(c->rank * slot * dtype_bytes(un.dtype));
     // Move(GPU2CPU) + Send + Receive, fused over NVLS when the gather buffer is symmetric
@@ -471,7 +471,7 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   // Every rank must reconstruct with the same kernel (tensor-core vs SIMT results differ in the
   // last bits) and pick the same gather protocol: decide from rank-invariant inputs only, and
   // reject a W the tensor-core plan cannot address instead of silently falling back on one rank.
-  if (c->world > 1 && scheme == POS_SCHEME_SFB && dtype != POS_DT_F32 && (N % 4) == 0)
+  if (c->world > 1 && scheme == POS_SCHEME_SFB && (N % 4) == 0)
     POS_CHECK_ARG(aligned16(W), "W must be 16-byte aligned (P > 1, tensor-core reconstruction)");
   if (scheme == POS_SCHEME_PS) {
     POS_CHECK_ARG(grad, "FC layer on the PS path needs a grad buffer");
@@ -487,9 +487,9 @@ int pos_sched_add_fc(pos_sched* s, int32_t l, int64_t M, int64_t N, int64_t K, i
   u.members = {l};
   if (scheme == POS_SCHEME_SFB) {
     u.sfb_idx = s->n_sfb++;
-    if (dtype != POS_DT_F32 && sfb_tc_would_pair(K * c->world, c->world == 1)) s->any_pair = true;
+    if (sfb_tc_would_pair(K * c->world * rows_per_sample(dtype), c->world == 1)) s->any_pair = true;
   }
-  const int64_t rows = scheme == POS_SCHEME_SFB ? K * c->world : K;
+  const int64_t rows = (scheme == POS_SCHEME_SFB ? K * c->world : K) * rows_per_sample(dtype);
   size_t bytes = (size_t)(rows * row_elems(M, N) * dtype_bytes(dtype));
   if (scheme == POS_SCHEME_SFB && c->world > 1 && !c->local && (s->flags & POS_SCHED_NO_SYMM) == 0) {
     // gather buffer in symmetric memory: the factors are multicast straight into it (collective,

@@ -1,8 +1,9 @@
-// A4 (POS_DT_F32): exact-fp32 SFB reconstruct-and-apply on the CUDA cores.
+// A4 fallback: SFB reconstruct-and-apply on the CUDA cores, for a W the TMA path cannot address
+// (N % 4 != 0, ldw % 4 != 0 or W not 16-byte aligned), any dtype.
 //   W[m][n] = (accumulate ? W[m][n] : 0) + alpha * sum_{j<KP} U[j][m] * V[j][n]
-// tcgen05 has no fp32-input kind (reading S16), so the "pure fp32" mode is a shared-memory tiled
-// FFMA GEMM with fp32 accumulation in a fixed k order. Also used for BF16/TF32 factors when the
-// caller's W cannot be addressed by TMA (ldw % 4 != 0 or W not 16-byte aligned).
+// over KP gathered ROWS (for POS_DT_F32 the 3xTF32 rows: the same three-term sum the tensor-core
+// path takes, reading S16). Shared-memory tiled FFMA GEMM, fp32 accumulation in a fixed k order.
+// (Round 1-2 ran POS_DT_F32 here for every shape: 340 us for VGG fc6 at K*P = 32, 0.37 of HBM.)
 // Tile 128 x 128, BK 16, 256 threads, 8 x 8 outputs per thread.
 #include <cuda_bf16.h>
 

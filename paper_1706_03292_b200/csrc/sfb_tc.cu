@@ -894,10 +894,11 @@ bool sfb_tc_supported(int64_t N, int64_t ldw, const float* W, const void* G) {
 bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t dtype,
                       const void* G, float* W, int64_t ldw, int max_ctas, float* bias,
                       const void* G2, bool cluster_ok) {
-  if (dtype == POS_DT_F32 || !sfb_tc_supported(N, ldw, W, G)) return false;
+  if (!sfb_tc_supported(N, ldw, W, G)) return false;
   if (G2 && !aligned16(G2)) return false;
-  if (dtype == POS_DT_TF32)
-    return make_plan_impl<true>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2, cluster_ok);
+  if (dtype != POS_DT_BF16)   // TF32, and F32 as the tf32 kind over 3 rows per pair (3xTF32)
+    return make_plan_impl<true>(pl, M, N, KP * rows_per_sample(dtype), G, W, ldw, max_ctas, bias,
+                                G2, cluster_ok);
   return make_plan_impl<false>(pl, M, N, KP, G, W, ldw, max_ctas, bias, G2, cluster_ok);
 }
 

@@ -280,7 +280,10 @@ __global__ void __launch_bounds__(kPsThreads, 2) ps_sync_kernel(PsArgs a, Xg x) 
 struct PackArgs {
   const void* u;
   const void* v;
-  int64_t M, N, Mp, R, K;
+  int64_t M, N, Mp, R;
+  int64_t K;                     // gathered rows of the slot (pairs * rows_per_sample)
+  int64_t Kp;                    // factor pairs
+  int split;                     // POS_DT_F32: 3xTF32 blocks (common.h, rows_per_sample)
   char* mc[2];                   // multicast address of the slot (kMc)
   char* dst[2][kMaxPeers];       // the slot in every rank's buffer (unicast / loopback)
   uint32_t* flag_mc;             // multicast address of flag[rank] (flag mode, kMc)
@@ -314,16 +317,19 @@ __global__ void __launch_bounds__(256) pack_x_kernel(PackArgs a, Xg x) {
   const int64_t chunks_per_row = a.R / VEC, total = a.K * chunks_per_row;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = c / chunks_per_row, col = (c % chunks_per_row) * VEC;
+    const int64_t r = c / chunks_per_row, col = (c % chunks_per_row) * VEC;
+    const int64_t k = a.split ? r % a.Kp : r;     // gathered row r holds factor pair k
     const Tin* src;
     int64_t idx, lim;
     if (col < a.Mp) { src = u + k * a.M; idx = col; lim = a.M; }
     else            { src = v + k * a.N; idx = col - a.Mp; lim = a.N; }
     const int64_t onec = col < a.Mp ? -1 : a.N;   // ones column (fused bias), as in pack_kernel
-    const uint4 q = pack_chunk<Tin, kBF16>(src, idx, lim, onec);
+    uint4 q = pack_chunk<Tin, kBF16>(src, idx, lim, onec);
+    if constexpr (!kBF16)
+      if (a.split) q = tf32_split4(q, split_part(r / a.Kp, col >= a.Mp));
     const float4 o = make_float4(__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
                                  __uint_as_float(q.w));   // bit pattern only; stores do not convert
-    const int64_t boff = (k * a.R + col) * EB;   // byte offset of this vector in the slot
+    const int64_t boff = (r * a.R + col) * EB;   // byte offset of this vector in the slot
     if constexpr (kMc) {
       mm_st_v4(reinterpret_cast<float*>(a.mc[b] + boff), o);
     } else {
@@ -451,7 +457,7 @@ int pack_grid(int64_t M, int64_t N, int64_t K, int32_t dtype) {
     return v < 1 ? 1 : v;
   }();
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
-  return grid_for(K * (row_elems(M, N) / vec), 256, pack_ctas);
+  return grid_for(K * rows_per_sample(dtype) * (row_elems(M, N) / vec), 256, pack_ctas);
 }
 
 }  // namespace
@@ -642,7 +648,7 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   if (mc_off) return POS_OK;
   const int P = c->world;
   const int64_t R = row_elems(M, N), eb = dtype_bytes(dtype);
-  const size_t slot_bytes = (size_t)(K * R * eb);
+  const size_t slot_bytes = (size_t)(K * rows_per_sample(dtype) * R * eb);
   size_t off = 0, off2 = 0, offf = 0;
   const SymmWindow* wb = symm_find(c, gbuf, slot_bytes * P, &off);
   if (!wb) return POS_OK;
@@ -652,7 +658,8 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   if (flag_mode && (!wb2 || !wf)) return POS_OK;   // inconsistent registration: caller uses NCCL
   PackArgs a{};
   a.u = u; a.v = v;
-  a.M = M; a.N = N; a.Mp = m_pad(M); a.R = R; a.K = K;
+  a.M = M; a.N = N; a.Mp = m_pad(M); a.R = R;
+  a.K = K * rows_per_sample(dtype); a.Kp = K; a.split = dtype == POS_DT_F32;
   a.P = P;
   const size_t mine = (size_t)c->rank * slot_bytes;
   a.mc[0] = wb->mc + off + mine;
@@ -831,7 +838,7 @@ int pos_loop_fc_create(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t dtyp
   lf->M = M; lf->N = N; lf->K = K;
   lf->dtype = dtype;
   lf->flag_mode = fm;
-  lf->slot_bytes = (size_t)(K * row_elems(M, N) * dtype_bytes(dtype));
+  lf->slot_bytes = (size_t)(K * rows_per_sample(dtype) * row_elems(M, N) * dtype_bytes(dtype));
   lf->buf_bytes = (lf->slot_bytes * P + 255) & ~size_t(255);
   const size_t alloc = fm ? 2 * lf->buf_bytes + 256 : lf->buf_bytes;
   lf->buf.assign(P, nullptr);
@@ -890,7 +897,8 @@ int pos_loop_fc_sync(pos_loop_fc* lf, int32_t in_dtype, const void* const* u,
   cudaStream_t s = (cudaStream_t)stream;
   // A2 + A3: every rank packs its factors into its slot of every replica's gather buffer
   PackArgs a{};
-  a.M = lf->M; a.N = lf->N; a.Mp = m_pad(lf->M); a.R = row_elems(lf->M, lf->N); a.K = lf->K;
+  a.M = lf->M; a.N = lf->N; a.Mp = m_pad(lf->M); a.R = row_elems(lf->M, lf->N);
+  a.K = lf->K * rows_per_sample(lf->dtype); a.Kp = lf->K; a.split = lf->dtype == POS_DT_F32;
   a.P = P;
   const int grid = pack_grid(lf->M, lf->N, lf->K, lf->dtype);
   for (int r = 0; r < P; ++r) {

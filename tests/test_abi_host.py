@@ -117,6 +117,11 @@ def test_factor_row_layout():
     assert pos.pos_factor_row_elems(1, 1) == 64 + 64
     assert pos.pos_factor_row_elems(64, 64) == 64 + 128
     assert pos.pos_factor_row_elems(13, 7) == 64 + 64
+    # 3xTF32 (reading S16): F32 packs three rows per factor pair
+    assert pos.pos_factor_slot_rows(32, pos.POS_DT_BF16) == 32
+    assert pos.pos_factor_slot_rows(32, pos.POS_DT_TF32) == 32
+    assert pos.pos_factor_slot_rows(32, pos.POS_DT_F32) == 96
+    assert pos.lib().pos_factor_slot_rows(1, 7) == pos.POS_EINVAL
 
 
 def test_b200_time_model_matches_oracle():

@@ -36,21 +36,22 @@ def test_reconstruct_writes_only_its_tile(dtype, M, N, K, extra_cols):
     Wv[:, :N] = to_dev(W)
     # gather buffer: packed rows for both workers, with its own guards
     R = pos.pos_factor_row_elems(M, N)
+    S = pos.pos_factor_slot_rows(K, pos.DTYPES[dtype]) * R      # one worker's slot (f32: 3K rows)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
-    gbuf = torch.zeros(G0 + P * K * R + G0, dtype=tdt, device="cuda")
+    gbuf = torch.zeros(G0 + P * S + G0, dtype=tdt, device="cuda")
     gbuf[:G0] = 7.0
-    gbuf[G0 + P * K * R:] = 7.0
+    gbuf[G0 + P * S:] = 7.0
     for p in range(P):
-        slot = gbuf[G0 + p * K * R: G0 + (p + 1) * K * R]
+        slot = gbuf[G0 + p * S: G0 + (p + 1) * S]
         st = "bf16" if dtype == "bf16" else "f32"
         pos.pos_pack_factors(to_dev(Us[p], st), to_dev(Vs[p], st), slot, pos.DTYPES[dtype])
     b = torch.full((M + 2,), float(CANARY), device="cuda")
     bw = si.exact_weights(si.rng(72), M)
     b[1:M + 1] = to_dev(bw)
-    pos.pos_reconstruct_apply(M, N, K * P, pos.DTYPES[dtype], gbuf[G0:G0 + P * K * R], Wv, b[1:M + 1],
+    pos.pos_reconstruct_apply(M, N, K * P, pos.DTYPES[dtype], gbuf[G0:G0 + P * S], Wv, b[1:M + 1],
                               si.EXACT_ALPHA, ldw=ldw)
     torch.cuda.synchronize()
-    assert bool(torch.all(gbuf[:G0] == 7.0)) and bool(torch.all(gbuf[G0 + P * K * R:] == 7.0))
+    assert bool(torch.all(gbuf[:G0] == 7.0)) and bool(torch.all(gbuf[G0 + P * S:] == 7.0))
     assert bool(canary_bits(buf[:G0]).all()) and bool(canary_bits(buf[G0 + M * ldw:]).all())
     if extra_cols:
         assert bool(canary_bits(Wv[:, N:]).all())

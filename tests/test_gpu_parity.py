@@ -92,7 +92,8 @@ def test_c0_sfb_equals_ps_exact_bitwise(P, dtype):
     grads = []
     R = pos.pos_factor_row_elems(M, N)
     for u, v in zip(Us, Vs):
-        slot = torch.empty(K * R, dtype=torch.bfloat16 if dtype == "bf16" else torch.float32, device="cuda")
+        rows = pos.pos_factor_slot_rows(K, pos.DTYPES[dtype])
+        slot = torch.empty(rows * R, dtype=torch.bfloat16 if dtype == "bf16" else torch.float32, device="cuda")
         pos.pos_pack_factors(to_dev(u, st), to_dev(v, st), slot, pos.DTYPES[dtype])
         gd = torch.empty(M * N, dtype=torch.float32, device="cuda")
         pos.pos_reconstruct_apply(M, N, K, pos.DTYPES[dtype], slot, gd, None, 1.0, accumulate=False)
@@ -275,7 +276,14 @@ def test_dense_ps_one_gpu_world1():
 
 
 # -------------------------------------------------------------------------------- pack A2 ----
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def _tf32_rna(x):
+    """fp32 -> tf32 (10 explicit mantissa bits), round to nearest with ties away from zero: add half
+    a tf32 ulp to the magnitude bits and truncate (IEEE sign-magnitude; finite inputs)."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return (((b + 0x1000) & 0xFFFFE000).astype(np.uint32)).view(np.float32)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32", "f32"])
 def test_pack_layout(dtype):
     K, M, N = 5, 13, 7
     g = si.rng(14)
@@ -283,13 +291,26 @@ def test_pack_layout(dtype):
     v = g.standard_normal((K, N)).astype(np.float32)
     R = pos.pos_factor_row_elems(M, N)
     assert R == 64 + 64
+    rows = pos.pos_factor_slot_rows(K, pos.DTYPES[dtype])
+    assert rows == (3 * K if dtype == "f32" else K)
     ud, vd = to_dev(u), to_dev(v)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
-    slot = torch.full((K, R), 99.0, dtype=tdt, device="cuda")
+    slot = torch.full((rows, R), 99.0, dtype=tdt, device="cuda")
     pos.pos_pack_factors(ud, vd, slot, pos.DTYPES[dtype])
     torch.cuda.synchronize()
-    exp = torch.zeros(K, R, dtype=tdt)
-    exp[:, :M] = torch.from_numpy(u).to(tdt)          # torch's CPU RNE cast
-    exp[:, 64:64 + N] = torch.from_numpy(v).to(tdt)
-    exp[:, 64 + N] = 1.0                              # ones column (fused bias gradient)
+    exp = torch.zeros(rows, R, dtype=tdt)
+    if dtype != "f32":
+        exp[:, :M] = torch.from_numpy(u).to(tdt)          # torch's CPU RNE cast (bf16); fp32 copy
+        exp[:, 64:64 + N] = torch.from_numpy(v).to(tdt)
+        exp[:, 64 + N] = 1.0                              # ones column (fused bias gradient)
+    else:
+        # 3xTF32 blocks (reading S16): (hi u, hi v), (hi u, lo v), (lo u, hi v)
+        hi = {"u": _tf32_rna(u), "v": _tf32_rna(v)}
+        lo = {"u": _tf32_rna(u - hi["u"]), "v": _tf32_rna(v - hi["v"])}
+        assert np.all(np.abs(hi["u"] + lo["u"] - u) <= 2.0 ** -21 * np.abs(u))
+        for blk, (pu, pv, one) in enumerate([(hi, hi, 1.0), (hi, lo, 0.0), (lo, hi, 1.0)]):
+            r = slice(blk * K, (blk + 1) * K)
+            exp[r, :M] = torch.from_numpy(pu["u"])
+            exp[r, 64:64 + N] = torch.from_numpy(pv["v"])
+            exp[r, 64 + N] = one
     assert torch.equal(slot.cpu(), exp)
