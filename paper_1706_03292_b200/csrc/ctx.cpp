@@ -56,10 +56,13 @@ int ctx_workspace(pos_ctx* c, size_t bytes, void** out) {
 }
 
 // A5 + A6 + A7 + A8 for a dense (or flattened FC) layer of n parameters, on stream s.
-int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W) {
+int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W, void* ce_buf) {
   const int P = c->world;
   if (P > 1 && !c->local) {
     const int64_t padded = pos_padded_size(n, P);
+    if (ce_buf && symm_lookup(c, W, (size_t)padded * 4) &&
+        symm_lookup(c, ce_buf, (size_t)symm_ce_bytes(n, P)))
+      return symm_ce_grid(c, n);
     if (symm_lookup(c, grad, (size_t)padded * 4) && symm_lookup(c, W, (size_t)padded * 4))
       return symm_ps_grid(c, n);
   }
@@ -70,13 +73,21 @@ int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W) {
 
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                    cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail, KTrace tr,
-                   KTrace tg, int lane) {
+                   KTrace tg, int lane, void* ce_buf, uint32_t* exit_word, bool* deferred) {
+  if (deferred) *deferred = false;
   const int P = c->world;
   const int64_t S = pos_shard_stride(n, P);
   if (S < 0) return (int)S;
+  if (ce_buf) {  // copy-engine transport (POS_PS_CE)
+    bool done = false;
+    int rc = symm_ps_ce(c, n, grad, W, ce_buf, alpha, s, ev_rs_done, ev_apply_done, &done, tr, tg);
+    if (rc != POS_OK || done) return rc;
+  }
   {  // NVLS fused kernel when grad and W live in symmetric memory (NEXT-1)
     bool done = false;
-    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done, tr, tg, lane);
+    int rc = symm_ps_fused(c, n, grad, W, alpha, s, ev_rs_done, ev_apply_done, &done, tr, tg, lane,
+                           exit_word);
+    if (deferred) *deferred = done && exit_word != nullptr;
     if (rc != POS_OK || done) return rc;
   }
   const int64_t padded = S * P;
@@ -193,6 +204,7 @@ static int ctx_common_init(pos_ctx* c) {
     const int64_t o = env_int("POS_REDUCE_ORDER", POS_REDUCE_AUTO);
     if (o == POS_REDUCE_SWITCH || o == POS_REDUCE_RANK_ORDER || o == POS_REDUCE_AUTO) c->reduce_order = (int)o;
   }
+  c->ps_ce = env_int("POS_PS_CE", 0) != 0 ? 1 : 0;
   const int64_t ms = env_int("POS_TIMEOUT_MS", 20000);
   c->timeout_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
   return POS_OK;

@@ -28,6 +28,10 @@ struct pos_ctx {
   int* err_dev = nullptr;
   unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
   int reduce_order = POS_REDUCE_AUTO;     // PS reduce: NVLS switch order, fixed rank order, auto
+  // PS transport of scheduler units (POS_PS_CE): 1 = the copy engines move the gradient pieces and
+  // the fresh shards (symm_ps_ce), 0 = the SM-driven fused kernel (symm_ps_fused). Fixed at context
+  // creation: the scheduler allocates the receive buffers at registration.
+  int ps_ce = 0;
   int fault = POS_FAULT_NONE, fault_rank = -1;   // fault injection (tests)
 };
 
@@ -48,11 +52,14 @@ inline ncclDataType_t nccl_type(int32_t dtype) {
 // stages shared by the one-shot entry points and the scheduler
 // zero_tail: zero grad[n, P*S) first (the one-shot API; the scheduler zeroes it once at add time
 // and the tail stays zero because the in-place reduce-scatter only ever sums zeros into it).
+// ce_buf: the unit's copy-engine receive buffer (symm_ce_bytes, from pos_mem_alloc) or nullptr
+// exit_word: defer the fused kernel's exit barrier (symm_ps_fused); *deferred tells whether it was
 int stage_ps_dense(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                    cudaEvent_t ev_rs_done, cudaEvent_t ev_apply_done, bool zero_tail,
-                   KTrace tr = {}, KTrace tg = {}, int lane = 0);
+                   KTrace tr = {}, KTrace tg = {}, int lane = 0, void* ce_buf = nullptr,
+                   uint32_t* exit_word = nullptr, bool* deferred = nullptr);
 // grid of the traced kernel stage_ps_dense launches for a unit of n parameters on this rank
-int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W);
+int ps_stage_grid(pos_ctx* c, int64_t n, float* grad, float* W, void* ce_buf = nullptr);
 int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype,
                         int32_t dtype, const void* u, const void* v, void* pack_buf, float* grad,
                         int32_t has_bias, cudaStream_t s);
@@ -61,10 +68,25 @@ int stage_fc_local_grad(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_
 void symm_destroy(pos_ctx* c);
 // fused reduce-scatter + apply + all-gather over NVLS when grad and W are symmetric; *done = false
 // (and nothing enqueued) otherwise
+// exit_word != nullptr: deferred exit (the kernel writes its epoch there; the caller completes the
+// unit with symm_ps_exit_wait on another stream, stream-ordered after this launch)
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
                   cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr = {},
-                  KTrace tg = {}, int lane = 0);
+                  KTrace tg = {}, int lane = 0, uint32_t* exit_word = nullptr);
+int symm_ps_exit_wait(pos_ctx* c, const uint32_t* exit_word, int lane, cudaStream_t s);
 constexpr int kMaxLanes = 2;
+// Copy-engine PS unit (POS_PS_CE): A6 as copy-engine pushes of this rank's gradient pieces into
+// their owners' receive buffers, A7 as a local kernel summing the P pieces in rank order into the
+// owned shard of W, A8 as copy-engine pushes of the fresh shard into every replica; completion is
+// signalled with release flags in the receive buffer's window and awaited with bounded polls.
+// Needs W (padded) symmetric and ce_buf = a symmetric allocation of symm_ce_bytes(n, P) bytes (one
+// per unit: the flags are reset-style, safe because a unit's iterations are stream-ordered on
+// every rank). *done = false (nothing enqueued) otherwise.
+int symm_ps_ce(pos_ctx* c, int64_t n, float* grad, float* W, void* ce_buf, float alpha,
+               cudaStream_t s, cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr = {},
+               KTrace tg = {});
+int64_t symm_ce_bytes(int64_t n, int P);
+int symm_ce_grid(pos_ctx* c, int64_t n);
 // grid of the fused PS kernel for a unit of n parameters (rank-invariant)
 int symm_ps_grid(pos_ctx* c, int64_t n);
 // pack this rank's factors and multicast them into every rank's gather buffer when the gather

@@ -30,8 +30,9 @@
 
 namespace {
 
-constexpr int kPool = 7;    // apply streams: [0], [4], [6] reconstructions; [1..3] dense applies;
-                             // [5] flag-mode factor packs (high priority)
+constexpr int kPool = 8;    // apply streams: [0], [4], [6] reconstructions; [1..3] dense applies;
+                             // [5] flag-mode factor packs (high priority); [7] completion of
+                             // the PS units with a deferred exit barrier (high priority)
 constexpr int kTRing = 4;   // timing event sets per unit (iterations in flight)
 
 struct TSlot {
@@ -57,6 +58,9 @@ struct Unit {
   void* gbuf2 = nullptr;
   uint32_t* gflags = nullptr;
   unsigned* gstate = nullptr;
+  void* ce_buf = nullptr;      // PS over the copy engines (ctx->ps_ce): receive slots + flags
+  uint32_t* exit_word = nullptr;   // fused PS kernel with a deferred exit: its epoch (device)
+  cudaEvent_t ev_issued = nullptr; // ... recorded after its launch; the exit wait follows it
   pos::SfbTcPlan plan;         // cached TMA descriptors of the tensor-core reconstruction
   bool has_plan = false;
   int plan_ctas = -1;
@@ -109,6 +113,7 @@ struct pos_sched {
   // -4%, but VGG19-22K +7% and AlexNet +17% (the packs gate the reconstructions there and slow
   // down next to the PS kernels) — off by default
   bool pack_stream = false;
+  bool defer_exit = true;   // POS_PS_DEFER=0: the fused PS kernels wait at their exit barrier
   int n_sfb = 0;              // SFB units registered
   bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
   // POS_SCHED_TRACE: one group record per scheme (all of a step's PS / SFB apply kernels)
@@ -153,7 +158,7 @@ int prepare_tracing(pos_sched* s) {
     if (un.scheme == POS_SCHEME_SFB)
       un.trace_grid = un.has_plan ? un.plan.grid : 0;        // the SIMT path is not traced
     else
-      un.trace_grid = ps_stage_grid(c, un.n, un.grad, un.W);
+      un.trace_grid = ps_stage_grid(c, un.n, un.grad, un.W, un.ce_buf);
     if (un.trace_grid > 0) exp[sc] += (unsigned)un.trace_grid;
     else if (un.scheme == POS_SCHEME_SFB) complete[sc] = false;
   }
@@ -351,12 +356,24 @@ int issue_unit(pos_sched* s, int ui) {
       if (ev_wfree != l0.ev_in) POS_CUDA_TRY(cudaStreamWaitEvent(cs, ev_wfree, 0));
     }
     if (ts && (rc = trec(ts->packed, cs))) return rc;
+    bool deferred = false;
     rc = stage_ps_dense(c, un.n, un.grad, un.W, s->alpha, cs, ts ? ts->a0 : nullptr,
                         ts ? ts->a1 : nullptr, /*zero_tail=*/false, unit_trace(s, un),
-                        group_trace(s, POS_SCHEME_PS), lane);
+                        group_trace(s, POS_SCHEME_PS), lane, un.ce_buf, un.exit_word, &deferred);
     if (rc != POS_OK) return rc;
-    if (ts && (rc = trec(ts->done, cs))) return rc;
-    POS_CUDA_TRY(cudaEventRecord(un.ev_done, cs));
+    if (deferred) {
+      // the lane's next unit starts right away; the unit is complete once every rank's shard has
+      // landed, which the exit wait on the completion stream establishes
+      cudaStream_t ds = s->pool[7];
+      POS_CUDA_TRY(cudaEventRecord(un.ev_issued, cs));
+      POS_CUDA_TRY(cudaStreamWaitEvent(ds, un.ev_issued, 0));
+      if ((rc = symm_ps_exit_wait(c, un.exit_word, lane, ds))) return rc;
+      if (ts && (rc = trec(ts->done, ds))) return rc;
+      POS_CUDA_TRY(cudaEventRecord(un.ev_done, ds));
+    } else {
+      if (ts && (rc = trec(ts->done, cs))) return rc;
+      POS_CUDA_TRY(cudaEventRecord(un.ev_done, cs));
+    }
   }
   return POS_OK;
 }
@@ -386,6 +403,19 @@ int new_unit(pos_sched* s, Unit&& u, int* out) {
   const bool tf = timing_full(s), ta = timing_any(s);
   int rc;
   if ((rc = make_event(&u.ev_gathered, false)) || (rc = make_event(&u.ev_done, false))) return rc;
+  pos_ctx* c = s->ctx;
+  if (u.scheme == POS_SCHEME_PS && s->defer_exit && c->world > 1 && !c->local) {
+    POS_CUDA_TRY(cudaMalloc(&u.exit_word, sizeof(uint32_t)));
+    POS_CUDA_TRY(cudaMemset(u.exit_word, 0, sizeof(uint32_t)));
+    if ((rc = make_event(&u.ev_issued, false))) return rc;
+  }
+  if (u.scheme == POS_SCHEME_PS && c->ps_ce && c->world > 1 && !c->local &&
+      (s->flags & POS_SCHED_NO_SYMM) == 0 &&
+      symm_lookup(c, u.W, (size_t)pos_padded_size(u.n, c->world) * 4)) {
+    // collective (every rank registers the same units in the same order, and the test above
+    // depends on rank-invariant registration only)
+    if ((rc = pos_mem_alloc(c, symm_ce_bytes(u.n, c->world), &u.ce_buf))) return rc;
+  }
   if (ta)
     for (auto& t : u.ring) {
       if ((rc = make_event(&t.a0, true)) || (rc = make_event(&t.a1, true))) return rc;
@@ -435,12 +465,14 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
   if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = std::max(1, std::min(3, atoi(e)));
   if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] == '1';
+  if (const char* e = getenv("POS_PS_DEFER")) s->defer_exit = e[0] != '0';
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   for (int i = 0; i < kPool; ++i) {
-    cudaError_t e = cudaStreamCreateWithPriority(&s->pool[i], cudaStreamNonBlocking, i == 5 ? hi : lo);
+    cudaError_t e = cudaStreamCreateWithPriority(&s->pool[i], cudaStreamNonBlocking,
+                                                 (i == 5 || i == 7) ? hi : lo);
     if (e != cudaSuccess) { pos_sched_destroy(s); return ctx_cuda_fail(c, e, "stream create"); }
   }
   if (cudaEventCreateWithFlags(&s->ev_end, cudaEventDisableTiming) != cudaSuccess) {
@@ -888,6 +920,9 @@ int pos_sched_destroy(pos_sched* s) {
     if (un.tile_counter) cudaFree(un.tile_counter);
     if (un.trace) cudaFree(un.trace);
     if (un.gstate) cudaFree(un.gstate);
+    if (un.ce_buf) pos_mem_free(s->ctx, un.ce_buf);
+    if (un.exit_word) cudaFree(un.exit_word);
+    if (un.ev_issued) cudaEventDestroy(un.ev_issued);
   }
   for (auto st : s->pool)
     if (st) cudaStreamDestroy(st);

@@ -26,13 +26,15 @@
 // context's timeout writes a code into the context's host-mapped error word and the kernel returns;
 // the host reports it as the sticky error POS_ETIMEOUT (SURVEY §5 failure detection).
 //
-// Barriers: one ENTRY inbox and one EXIT inbox (u32 counters) per context in a symmetric window.
-// Entry: CTA 0 of each rank adds 1 to every rank's entry inbox (multimem.red); every CTA polls its
-// local inbox until all P arrivals of this kernel instance are in. Exit: each CTA counts itself done;
-// the LAST CTA of the rank adds 1 to every exit inbox (release) and waits for all P. No CTA waits
-// for a specific CTA of another GPU, so the kernels tolerate any residency pattern (a per-CTA-index
-// barrier needs matching CTAs of all GPUs co-resident at once). Fused kernels of one context must
-// be stream-ordered among themselves (the scheduler issues them all on its comm stream).
+// Barriers: per lane, P ENTRY and P EXIT epoch slots (u32) in a symmetric window; slot r holds the
+// epoch of rank r's latest kernel instance on the lane. Entry: CTA 0 of each rank multicasts its
+// epoch into slot r of every rank; every CTA polls its local slots until all P reach the instance's
+// epoch. Exit: each CTA counts itself done; the LAST CTA of the rank multicasts the epoch into the
+// exit slots (release) and waits for all P — or, for the scheduler's PS units, records the epoch
+// and leaves the wait to xg_exit_wait_kernel on a completion stream, so the next unit of the lane
+// starts without a cross-GPU round trip. No CTA waits for a specific CTA of another GPU, so the
+// kernels tolerate any residency pattern (a per-CTA-index barrier needs matching CTAs of all GPUs
+// co-resident at once). Fused kernels of one lane must be stream-ordered among themselves.
 #include <cuda_bf16.h>
 #include <nccl.h>
 #include <nccl_device.h>
@@ -65,7 +67,8 @@ static SymmState* state(pos_ctx* c) { return static_cast<SymmState*>(c->symm); }
 namespace {
 
 // error sites reported through the context's error word (see site_name)
-enum { kSitePsEntry = 1, kSitePsExit = 2, kSitePackEntry = 3, kSitePackExit = 4, kSiteFlags = 5 };
+enum { kSitePsEntry = 1, kSitePsExit = 2, kSitePackEntry = 3, kSitePackExit = 4, kSiteFlags = 5,
+       kSiteCeData = 6, kSiteCeShard = 7 };
 
 // ------------------------------------------------------------------------------ device -------
 __device__ __forceinline__ float4 mm_ld_reduce_v4(const float* p) {
@@ -122,34 +125,41 @@ __device__ bool poll_reached(const uint32_t* p, uint32_t target, unsigned long l
 
 // Cross-GPU synchronisation of one fused-kernel instance. local == nullptr: none (P = 1 or the
 // single-GPU loopback, where ranks run one after the other in stream order).
+// Every lane has a block of slots in the barrier window: entry slots [0, P) and exit slots
+// [kXgExit, kXgExit + P); slot r is written only by rank r, with the EPOCH of its latest kernel
+// instance on the lane (state[0] + 1: every rank runs the same instances in the same order). A wait
+// polls the P slots for >= the instance's epoch, so a rank that has already moved on to a later
+// instance still counts as arrived, and no rank can be mistaken for arrived before it was.
 struct Xg {
-  uint32_t* mc;          // multicast address of the inbox pair [entry, exit]
-  uint32_t* local;       // this rank's inbox pair
-  uint32_t* state;       // [0] entry epoch, [1] exit epoch, [2] CTAs of this instance done
-  int P;
+  uint32_t* mc;          // multicast address of this lane's slot block
+  uint32_t* local;       // this rank's copy of the slot block
+  uint32_t* state;       // [0] epoch of the lane's last instance, [2] CTAs of this instance done
+  uint32_t* exit_word;   // deferred exit: the epoch is written here and nobody waits (the caller
+                         // runs xg_exit_wait_kernel on another stream); nullptr = wait at exit
+  int P, rank;
   unsigned long long timeout_ns;
   int* err;
   int site;              // entry site; exit = site + 1
 };
+constexpr int kXgExit = kMaxPeers;    // exit slots follow the entry slots
+constexpr int kXgLaneBytes = 256;     // slot block of lane k at byte 256 k of the window
 
 // Entry: every rank's inputs (produced by kernels that completed in stream order) are in place.
 // The arrival needs no release fence: the data was written by completed kernels.
 __device__ __forceinline__ bool xg_enter(const Xg& x) {
-  __shared__ int s_ok;
   if (!x.local) return true;
-  if (threadIdx.x == 0) {
-    const uint32_t target = *reinterpret_cast<volatile uint32_t*>(x.state) + (uint32_t)x.P;
-    if (blockIdx.x == 0)
-      asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(x.mc) : "memory");
-    s_ok = poll_reached(x.local, target, x.timeout_ns, x.err, x.site) ? 1 : 0;
-  }
-  __syncthreads();
-  return s_ok != 0;
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(x.state) + 1u;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    asm volatile("multimem.st.relaxed.sys.global.u32 [%0], %1;" ::"l"(x.mc + x.rank), "r"(e)
+                 : "memory");
+  int ok = 1;
+  if (threadIdx.x < x.P) ok = poll_reached(x.local + threadIdx.x, e, x.timeout_ns, x.err, x.site);
+  return __syncthreads_and(ok) != 0;
 }
 
-// Exit: the last CTA of this rank (all of the rank's stores performed) signals with release and
-// waits until every rank has done the same — every replica's outputs are complete and every input
-// read, before any rank's stream moves on.
+// Exit: the last CTA of this rank (all of the rank's stores performed) publishes the epoch with
+// release into every rank's exit slot and — unless the exit is deferred — waits until every rank
+// has done the same: every replica's outputs are complete and every input read.
 __device__ __forceinline__ void xg_exit(const Xg& x) {
   if (!x.local) return;
   __syncthreads();
@@ -159,13 +169,26 @@ __device__ __forceinline__ void xg_exit(const Xg& x) {
     if (prev == gridDim.x - 1) {
       __threadfence_system();
       x.state[2] = 0;
-      const uint32_t target = x.state[1] + (uint32_t)x.P;
-      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(x.mc + 1) : "memory");
-      poll_reached(x.local + 1, target, x.timeout_ns, x.err, x.site + 1);
-      x.state[0] += (uint32_t)x.P;
-      x.state[1] = target;
+      const uint32_t e = x.state[0] + 1u;
+      asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(x.mc + kXgExit + x.rank),
+                   "r"(e)
+                   : "memory");
+      if (x.exit_word) {
+        *x.exit_word = e;
+      } else {
+        for (int t = 0; t < x.P; ++t)
+          poll_reached(x.local + kXgExit + t, e, x.timeout_ns, x.err, x.site + 1);
+      }
+      x.state[0] = e;
     }
   }
+}
+
+// The deferred exit of one instance (stream-ordered after it): every rank's outputs are complete.
+__global__ void xg_exit_wait_kernel(const uint32_t* local, const uint32_t* exit_word, int P,
+                                    unsigned long long timeout_ns, int* err, int site) {
+  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(exit_word);
+  if (threadIdx.x < P) poll_reached(local + kXgExit + threadIdx.x, e, timeout_ns, err, site);
 }
 
 constexpr int kPsThreads = 512;
@@ -378,6 +401,99 @@ __global__ void resolve_window_kernel(ncclDevComm dc, ncclWindow_t w, int P, cha
   }
 }
 
+// ------------------------------------------------------------------ copy-engine PS unit -----
+// The data moves on the copy engines (cudaMemcpyAsync into the peers' windows: ~770 GB/s per
+// direction at P = 2 on this pool against ~450 for SM-driven NVLink loads / stores, and no SMs
+// taken from the co-running reconstructions); these kernels only signal, wait and apply.
+// Receive window of a unit (symm_ce_bytes): [flag1: P u32 | pad][flag2: P u32 | pad] (4096 B),
+// then P slots of S floats: slot p = rank p's piece of this rank's shard. Flags are reset-style
+// (1 = arrived): each is reset by its consumer before the signal that lets the producer set it
+// again, so a constant value works under CUDA-graph replay.
+constexpr int64_t kCeHdr = 4096;
+
+struct CeSignal {
+  uint32_t* peer[kMaxPeers];   // flag[rank] in every peer's window (this rank's slot)
+  uint32_t* reset;             // this rank's flag row to reset first (nullptr = none)
+  int P, rank;
+};
+
+__global__ void ce_signal_kernel(CeSignal a) {
+  const int t = threadIdx.x;
+  if (a.reset) {
+    if (t < a.P) a.reset[t] = 0u;
+    __threadfence_system();
+    __syncthreads();
+  }
+  if (t < a.P && t != a.rank) {
+    __threadfence_system();   // the copies before this kernel in stream order are complete
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.peer[t]), "r"(1u) : "memory");
+  }
+}
+
+// bounded wait for the P-1 peers' flags of a row, then reset them (the fresh shards are in W)
+__global__ void ce_wait_kernel(uint32_t* flag, int P, int rank, unsigned long long timeout_ns,
+                               int* err) {
+  const int t = threadIdx.x;
+  if (t < P && t != rank && poll_reached(flag + t, 1u, timeout_ns, err, kSiteCeShard)) flag[t] = 0u;
+}
+
+struct CeApply {
+  const float* g;       // this rank's gradient, element 0 of the unit
+  const float* recv;    // this rank's receive slots (slot p at p * S)
+  float* W;             // this rank's W, element 0 of the unit
+  uint32_t* flag;       // this rank's flag1 row
+  int64_t S, lo, hi;
+  int P, rank;
+  float alpha;
+  unsigned long long timeout_ns;
+  int* err;
+  KTrace trace, group;
+};
+
+// A7 on the owned shard once every peer's piece has arrived: W[lo+i] += alpha * sum_p piece_p[i],
+// summed in rank order from piece 0 (the same arithmetic as the fused kernel's RANK_ORDER mode)
+__global__ void __launch_bounds__(256) ce_apply_kernel(CeApply a) {
+  ktrace_begin(a.trace);
+  ktrace_begin(a.group);
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < a.P && threadIdx.x != a.rank &&
+      !poll_reached(a.flag + threadIdx.x, 1u, a.timeout_ns, a.err, kSiteCeData))
+    s_ok = 0;
+  __syncthreads();
+  if (s_ok) {
+    const int64_t cnt = a.hi - a.lo, n4 = cnt / 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    auto piece = [&](int p) { return p == a.rank ? a.g + a.lo : a.recv + (int64_t)p * a.S; };
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      float4 s = reinterpret_cast<const float4*>(piece(0))[i];
+      for (int p = 1; p < a.P; ++p) {
+        const float4 t = reinterpret_cast<const float4*>(piece(p))[i];
+        s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+      }
+      float4* wp = reinterpret_cast<float4*>(a.W + a.lo) + i;
+      float4 w = *wp;
+      w.x = fmaf(a.alpha, s.x, w.x);
+      w.y = fmaf(a.alpha, s.y, w.y);
+      w.z = fmaf(a.alpha, s.z, w.z);
+      w.w = fmaf(a.alpha, s.w, w.w);
+      *wp = w;
+    }
+    if (blockIdx.x == 0)
+      for (int64_t j = n4 * 4 + threadIdx.x; j < cnt; j += blockDim.x) {
+        float s = piece(0)[j];
+        for (int p = 1; p < a.P; ++p) s += piece(p)[j];
+        a.W[a.lo + j] = fmaf(a.alpha, s, a.W[a.lo + j]);
+      }
+  }
+  if (a.trace.rec || a.group.rec) {
+    __syncthreads();
+    ktrace_end(a.trace);
+    ktrace_end(a.group);
+  }
+}
+
 int grid_for(int64_t items, int threads, int cap) {
   int64_t g = (items + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -403,16 +519,18 @@ int ps_grid(pos_ctx* c, int64_t n, int P) {
   return grid_for(std::max<int64_t>(1, S / 4 / kPsUnroll), kPsThreads, cap);
 }
 
-// lane k: inbox pair at byte offset 64 k of the barrier window, epochs at bar_state + 4 k
-Xg make_xg(pos_ctx* c, int site, int lane = 0) {
+// lane k: slot block at byte offset 256 k of the barrier window, epoch state at bar_state + 4 k
+Xg make_xg(pos_ctx* c, int site, int lane = 0, uint32_t* exit_word = nullptr) {
   Xg x{};
   SymmState* st = state(c);
   if (st && st->bar.mc && c->world > 1) {
-    x.mc = reinterpret_cast<uint32_t*>(st->bar.mc + 64 * lane);
-    x.local = reinterpret_cast<uint32_t*>(st->bar.base + 64 * lane);
+    x.mc = reinterpret_cast<uint32_t*>(st->bar.mc + kXgLaneBytes * lane);
+    x.local = reinterpret_cast<uint32_t*>(st->bar.base + kXgLaneBytes * lane);
     x.state = st->bar_state + 4 * lane;
+    x.exit_word = exit_word;
   }
   x.P = c->world;
+  x.rank = c->rank;
   x.timeout_ns = c->timeout_ns;
   x.err = c->err_dev;
   x.site = site;
@@ -470,6 +588,8 @@ const char* site_name(int site) {
     case kSitePackEntry: return "factor gather entry barrier";
     case kSitePackExit: return "factor gather exit barrier";
     case kSiteFlags: return "factor gather ready flags (a peer's slot never arrived)";
+    case kSiteCeData: return "copy-engine PS: a peer's gradient piece never arrived";
+    case kSiteCeShard: return "copy-engine PS: a peer's fresh shard never arrived";
     default: return "unknown cross-GPU wait";
   }
 }
@@ -589,8 +709,21 @@ bool symm_lookup(pos_ctx* c, const void* p, size_t bytes) {
 
 int symm_ps_grid(pos_ctx* c, int64_t n) { return ps_grid(c, n, c->world); }
 
+int symm_ps_exit_wait(pos_ctx* c, const uint32_t* exit_word, int lane, cudaStream_t s) {
+  SymmState* st = state(c);
+  if (!st || !st->bar.mc || c->world < 2) return POS_OK;
+  clear_stale_launch_error();
+  xg_exit_wait_kernel<<<1, 32, 0, s>>>(
+      reinterpret_cast<const uint32_t*>(st->bar.base + kXgLaneBytes * lane), exit_word, c->world,
+      c->timeout_ns, c->err_dev, kSitePsExit);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "xg_exit_wait_kernel launch");
+  return POS_OK;
+}
+
 int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cudaStream_t s,
-                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr, KTrace tg, int lane) {
+                  cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr, KTrace tg, int lane,
+                  uint32_t* exit_word) {
   *done = false;
   const int P = c->world;
   if (P < 2 || c->local) return POS_OK;
@@ -612,7 +745,7 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   a.trace = tr;
   a.group = tg;
   pos_shard_range(n, P, c->rank, &a.lo, &a.hi);
-  const Xg x = make_xg(c, kSitePsEntry, lane);
+  const Xg x = make_xg(c, kSitePsEntry, lane, exit_word);
   if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
   const int grid = ps_grid(c, n, P);
   // P = 2: plain peer loads (summed in rank order: deterministic) + unicast peer stores move n/2 +
@@ -632,6 +765,91 @@ int symm_ps_fused(pos_ctx* c, int64_t n, float* grad, float* W, float alpha, cud
   }
   if (e != cudaSuccess) return ctx_cuda_fail(c, e, "ps_sync_kernel launch");
   if (ev_a1) POS_CUDA_TRY(record_timing_event(ev_a1, s));
+  *done = true;
+  return POS_OK;
+}
+
+int64_t symm_ce_bytes(int64_t n, int P) { return kCeHdr + 4 * (int64_t)P * pos_shard_stride(n, P); }
+
+int symm_ce_grid(pos_ctx* c, int64_t n) {
+  int64_t lo = 0, hi = 0;
+  pos_shard_range(n, c->world, c->rank, &lo, &hi);
+  // at least one CTA: the apply kernel also consumes the peers' flags (an empty shard included)
+  return std::max(1, ps_apply_grid(hi - lo));
+}
+
+int symm_ps_ce(pos_ctx* c, int64_t n, float* grad, float* W, void* ce_buf, float alpha,
+               cudaStream_t s, cudaEvent_t ev_a0, cudaEvent_t ev_a1, bool* done, KTrace tr,
+               KTrace tg) {
+  *done = false;
+  const int P = c->world, r = c->rank;
+  if (P < 2 || c->local) return POS_OK;
+  const int64_t S = pos_shard_stride(n, P);
+  size_t ow = 0, oc = 0;
+  const SymmWindow* ww = symm_find(c, W, (size_t)(S * P) * 4, &ow);
+  const SymmWindow* wc = symm_find(c, ce_buf, (size_t)symm_ce_bytes(n, P), &oc);
+  if (!ww || !wc) return POS_OK;
+  if (ev_a0) POS_CUDA_TRY(record_timing_event(ev_a0, s));
+  if (c->fault == POS_FAULT_SKIP_PS && c->fault_rank == r) {   // never joins: peers time out
+    if (ev_a1) POS_CUDA_TRY(record_timing_event(ev_a1, s));
+    *done = true;
+    return POS_OK;
+  }
+  clear_stale_launch_error();
+  auto flag_at = [&](int q, int row) {   // flag[row][r] in rank q's window
+    return reinterpret_cast<uint32_t*>(wc->peer[q] + oc + 128 * row) + r;
+  };
+  // A6: push this rank's piece of every peer's shard into that peer's slot r
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    int64_t lo = 0, hi = 0;
+    pos_shard_range(n, P, q, &lo, &hi);
+    if (hi > lo) {
+      cudaError_t e = cudaMemcpyAsync(wc->peer[q] + oc + kCeHdr + 4 * (size_t)(r * S), grad + lo,
+                                      4 * (size_t)(hi - lo), cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return ctx_cuda_fail(c, e, "copy-engine push (gradient piece)");
+    }
+  }
+  CeSignal sg{};
+  for (int q = 0; q < P; ++q) sg.peer[q] = flag_at(q, 0);
+  sg.P = P;
+  sg.rank = r;
+  ce_signal_kernel<<<1, 32, 0, s>>>(sg);
+  // A7: wait for the peers' pieces, sum in rank order, apply to the owned shard
+  CeApply a{};
+  a.g = grad;
+  a.recv = reinterpret_cast<const float*>(wc->base + oc + kCeHdr);
+  a.W = W;
+  a.flag = reinterpret_cast<uint32_t*>(wc->base + oc);
+  a.S = S;
+  pos_shard_range(n, P, r, &a.lo, &a.hi);
+  a.P = P;
+  a.rank = r;
+  a.alpha = alpha;
+  a.timeout_ns = c->timeout_ns;
+  a.err = c->err_dev;
+  a.trace = tr;
+  a.group = tg;
+  const int grid = symm_ce_grid(c, n);
+  if (a.trace.rec && a.trace.expected == 0) a.trace.expected = (unsigned)grid;
+  ce_apply_kernel<<<grid, 256, 0, s>>>(a);
+  if (ev_a1) POS_CUDA_TRY(record_timing_event(ev_a1, s));
+  // A8: push the fresh shard into every replica, then signal (resetting this rank's flag1 row:
+  // every apply CTA has consumed it) and wait for every peer's shard
+  if (a.hi > a.lo)
+    for (int q = 0; q < P; ++q) {
+      if (q == r) continue;
+      cudaError_t e = cudaMemcpyAsync(ww->peer[q] + ow + 4 * (size_t)a.lo, W + a.lo,
+                                      4 * (size_t)(a.hi - a.lo), cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return ctx_cuda_fail(c, e, "copy-engine push (fresh shard)");
+    }
+  for (int q = 0; q < P; ++q) sg.peer[q] = flag_at(q, 1);
+  sg.reset = a.flag;
+  ce_signal_kernel<<<1, 32, 0, s>>>(sg);
+  ce_wait_kernel<<<1, 32, 0, s>>>(reinterpret_cast<uint32_t*>(wc->base + oc + 128), P, r,
+                                  c->timeout_ns, c->err_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "copy-engine PS kernels");
   *done = true;
   return POS_OK;
 }
@@ -718,6 +936,10 @@ cudaError_t preload_symm_kernels() {
       POS_PK(float, false, false, false),
 #undef POS_PK
       reinterpret_cast<const void*>(wait_flags_kernel),
+      reinterpret_cast<const void*>(xg_exit_wait_kernel),
+      reinterpret_cast<const void*>(ce_signal_kernel),
+      reinterpret_cast<const void*>(ce_wait_kernel),
+      reinterpret_cast<const void*>(ce_apply_kernel),
       reinterpret_cast<const void*>(resolve_window_kernel)};
   for (const void* f : fns)
     if (cudaError_t e = cudaFuncGetAttributes(&fa, f); e != cudaSuccess) return e;

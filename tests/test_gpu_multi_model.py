@@ -119,6 +119,14 @@ def _worker(rank, world, port, outdir):
             del os.environ["POS_PS_LANES"]
         full_model(ctx_l, "vgg19_22k_lanes2")
         ctx_l.close()
+        # the same with the PS units on the copy engines (POS_PS_CE: pushes + flags + local apply)
+        os.environ["POS_PS_CE"] = "1"
+        try:
+            ctx_ce = pos.Context.from_torch_distributed()
+        finally:
+            del os.environ["POS_PS_CE"]
+        full_model(ctx_ce, "vgg19_22k_ce")
+        ctx_ce.close()
 
         # ---- (b) PS determinism: switch order (recorded) and rank order (asserted) ----------------
         n = 2359808 * 4 + 4097
