@@ -112,7 +112,7 @@ struct pos_sched {
   // chain then starts with the first dense unit. Measured at P = 2 (round 2): VGG19 -7%, IncV3
   // -4%, but VGG19-22K +7% and AlexNet +17% (the packs gate the reconstructions there and slow
   // down next to the PS kernels) — off by default
-  bool pack_stream = false;
+  int pack_stream = -1;     // flag-mode packs on pool[5]: 1 / 0 forced (POS_PACK_STREAM), -1 auto
   bool defer_exit = true;   // POS_PS_DEFER=0: the fused PS kernels wait at their exit barrier
   int n_sfb = 0;              // SFB units registered
   bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
@@ -262,7 +262,7 @@ int issue_unit(pos_sched* s, int ui) {
   // Flag-mode packs (multicast stores + ready flags, no cross-GPU barrier) need no ordering with
   // the fused PS kernels, which keep the comm stream to themselves: the PS chain then starts
   // with the first dense unit instead of queueing behind every factor pack of the step
-  if (coll && un.scheme == POS_SCHEME_SFB && un.flag_mode && s->pack_stream) cs = s->pool[5];
+  if (coll && un.scheme == POS_SCHEME_SFB && un.flag_mode && s->pack_stream == 1) cs = s->pool[5];
   // PS units alternate between the context's lanes by registration order (identical on every rank)
   const int lane = (coll && un.scheme != POS_SCHEME_SFB && c->ps_lanes > 1) ? un.seq % c->ps_lanes : 0;
   if (lane > 0) cs = c->lane_stream[lane];
@@ -464,7 +464,7 @@ int pos_sched_create(pos_ctx* c, int32_t n_layers, int32_t flags, pos_sched** ou
   s->flags = flags;
   s->ps_after_sfb = (flags & POS_SCHED_PS_AFTER_SFB) != 0;
   if (const char* e = getenv("POS_SFB_STREAMS")) s->sfb_streams = std::max(1, std::min(3, atoi(e)));
-  if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] == '1';
+  if (const char* e = getenv("POS_PACK_STREAM")) s->pack_stream = e[0] == '1' ? 1 : 0;
   if (const char* e = getenv("POS_PS_DEFER")) s->defer_exit = e[0] != '0';
   s->layers.resize(n_layers);
   s->units.reserve(n_layers);
@@ -602,6 +602,21 @@ int pos_sched_begin(pos_sched* s, float alpha) {
   int rc = ctx_check(s->ctx);
   if (rc) return rc;
   if (tracing(s) && (rc = prepare_tracing(s))) return rc;
+  if (s->pack_stream < 0) {
+    // Which chain is the long pole: the PS units' NVLink transfers or the reconstructions' HBM
+    // streams? If the PS chain is, the factor packs leave the comm stream so the first PS unit
+    // starts at once (measured, P = 2 / 4: VGG19 -9% / -5%, Inception-V3 -5% / -4%); otherwise
+    // they stay ahead of the PS units so every reconstruction can start early (VGG19-22K +2% / +5%,
+    // AlexNet +14% / +25% with the packs moved). Rank-invariant: registered units only.
+    constexpr double kNvlBps = 500e9, kHbmBps = 6551e9;   // per direction (measured, P = 2..4)
+    const double P = (double)s->ctx->world;
+    double t_ps = 0.0, t_sfb = 0.0;
+    for (const auto& un : s->units) {
+      if (un.scheme == POS_SCHEME_SFB) t_sfb += 8.0 * (double)un.M * (double)un.N / kHbmBps;
+      else t_ps += 8.0 * (P - 1.0) / P * (double)un.n / kNvlBps;
+    }
+    s->pack_stream = t_ps > t_sfb ? 1 : 0;
+  }
   for (auto& ly : s->layers) ly.triggered = false;   // C := 0
   for (auto& un : s->units) un.pending = (int)un.members.size();
   s->order.clear();
