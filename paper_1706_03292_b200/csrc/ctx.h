@@ -13,7 +13,7 @@ struct pos_ctx {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;  // high-priority stream for collectives (scheduler)
   // fused PS units may run on up to kMaxLanes concurrent LANES: each lane has its own stream and
-  // its own cross-GPU barrier inbox / epochs, so units of different lanes overlap while each lane
+  // its own cross-GPU barrier slots / epoch, so units of different lanes overlap while each lane
   // stays stream-ordered (POS_PS_LANES; the scheduler assigns lanes by unit registration order)
   cudaStream_t lane_stream[2] = {nullptr, nullptr};   // [0] = comm_stream
   int ps_lanes = 1;
