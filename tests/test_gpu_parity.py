@@ -179,15 +179,28 @@ def test_pair_and_single_kernels_statistical_large_kp(pair, dtype, monkeypatch):
 
 
 # ---------------------------------------------------------------------- full-size layers ----
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("layer", [(4096, 25088, 32, 1), (21841, 4096, 32, 1), (4096, 4096, 32, 8),
                                    (1000, 4096, 32, 2)])
-def test_full_size_layers_exact_bitwise(layer):
+def test_full_size_layers_exact_bitwise(layer, dtype):
     """Bench shapes (C3 VGG19-22K fc6/fc8 at P = 1; fc7 at K*P = 256), launched exactly as the bench
-    launches them (tensor-core kernel, one CTA per SM), compared element by element."""
+    launches them (tensor-core kernel, one CTA per SM), compared element by element. f32: the 3xTF32
+    rows (3 K P of them) through the same kernel."""
     M, N, K, P = layer
-    _, _, Wg, bg, Wr, br = run_sfb(P, K, M, N, "bf16", "bf16", "exact", seed=11)
+    _, _, Wg, bg, Wr, br = run_sfb(P, K, M, N, dtype, "bf16" if dtype == "bf16" else "f32", "exact", seed=11)
     assert np.array_equal(Wg, Wr)
     assert np.array_equal(bg, br)
+
+
+@pytest.mark.parametrize("layer", [(4096, 25088, 32, 1), (21841, 4096, 32, 2)])
+def test_full_size_f32_statistical(layer):
+    """fp32 factors (3xTF32, reading S16) at the bench's largest shapes, statistical regime: every
+    element of W' and dW within the fp32 tolerance of the fp64 oracle."""
+    M, N, K, P = layer
+    W, b, Wg, bg, Wr, br = run_sfb(P, K, M, N, "f32", "f32", "stat", seed=12)
+    assert err(Wg, Wr) <= TOL["f32"]
+    assert err(Wg - W, Wr - W) <= TOL["f32"]
+    assert err(bg - b, br - b) <= TOL["f32"]
 
 
 def test_alexnet_kp1024_full():
