@@ -112,6 +112,8 @@ def parse():
     a = ap.parse_args()
     if a.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if a.dtype == "f32" and os.environ.get("POS_F32_FFMA") == "1":
+        a.no_trace = True    # exact-fp32 mode: SIMT reconstruction, not traced — CUDA-event timing
     return a
 
 

@@ -145,7 +145,9 @@ int64_t pos_factor_row_elems(int64_t M, int64_t N);
  * 3xTF32 on the tensor cores (reading S16): the pair k is packed as rows k, K+k, 2K+k holding
  * (tf32(u), tf32(v)), (tf32(u), lo(v)), (lo(u), tf32(v)) with lo(x) = tf32(x - tf32(x)); tf32() rounds
  * to nearest, ties away. The contraction over the three rows is u^T v up to the lo(u) lo(v) term and
- * the rounding of lo (relative error ~2^-21 per product). Negative on bad arguments. */
+ * the rounding of lo (relative error ~2^-21 per product). POS_F32_FFMA=1 in the environment (read
+ * once per process) selects the exact-fp32 mode instead: K rows, SIMT FFMA reconstruction.
+ * Negative on bad arguments. */
 int64_t pos_factor_slot_rows(int64_t K, int32_t dtype);
 
 /* ======================================================================================

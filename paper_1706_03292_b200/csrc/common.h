@@ -58,7 +58,16 @@ inline int64_t dtype_bytes(int32_t dtype) { return dtype == POS_DT_BF16 ? 2 : 4;
 // (reading S16): the pack writes each pair three times, as K-row blocks (hi u, hi v),
 // (hi u, lo v), (lo u, hi v) with hi = tf32(x), lo = tf32(x - hi), so one tf32 contraction over
 // 3K rows per slot gives sum_k hi·hi + hi·lo + lo·hi = u_k^T v_k up to the dropped lo·lo term.
-inline int64_t rows_per_sample(int32_t dtype) { return dtype == POS_DT_F32 ? 3 : 1; }
+// POS_F32_FFMA=1 (read once per process) keeps the rounds-1/2 exact-fp32 mode instead: one row per
+// pair and the SIMT FFMA reconstruction.
+inline bool f32_ffma() {
+  static const bool v = [] {
+    const char* e = getenv("POS_F32_FFMA");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+inline int64_t rows_per_sample(int32_t dtype) { return dtype == POS_DT_F32 && !f32_ffma() ? 3 : 1; }
 
 int num_sms();
 

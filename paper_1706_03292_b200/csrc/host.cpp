@@ -236,7 +236,7 @@ int reconstruct_apply(int64_t M, int64_t N, int64_t KP, int32_t dtype, const voi
   POS_CHECK_ARG(aligned16(G), "G must be 16-byte aligned");
   POS_CHECK_ARG((M * ldw) / ldw == M, "M * ldw overflows");
   cudaError_t e;
-  const bool tc = sfb_tc_supported(N, ldw, W, G);
+  const bool tc = sfb_tc_supported(N, ldw, W, G) && !(dtype == POS_DT_F32 && f32_ffma());
   const int64_t rows = KP * rows_per_sample(dtype);   // 3xTF32 rows for POS_DT_F32
   if (tc) {   // bias fused into the tensor-core epilogue (ones column)
     e = launch_sfb_tc(M, N, KP, dtype, G, accumulate, W, ldw, b, alpha, max_ctas, s);

@@ -171,7 +171,7 @@ cudaError_t launch_pack_factors(int64_t M, int64_t N, int64_t K, int32_t in_dtyp
   const int vec = dtype == POS_DT_BF16 ? 8 : 4;
   const int64_t chunks = R / vec;
   const int64_t rows = K * rows_per_sample(dtype);
-  const int split = dtype == POS_DT_F32;
+  const int split = rows_per_sample(dtype) == 3;
   for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
     const unsigned nr = (unsigned)std::min<int64_t>(65535, rows - r0);
     dim3 grid((unsigned)((chunks + threads - 1) / threads), nr);

@@ -895,6 +895,7 @@ bool sfb_tc_make_plan(SfbTcPlan* pl, int64_t M, int64_t N, int64_t KP, int32_t d
                       const void* G, float* W, int64_t ldw, int max_ctas, float* bias,
                       const void* G2, bool cluster_ok) {
   if (!sfb_tc_supported(N, ldw, W, G)) return false;
+  if (dtype == POS_DT_F32 && f32_ffma()) return false;   // exact-fp32 mode: SIMT FFMA
   if (G2 && !aligned16(G2)) return false;
   if (dtype != POS_DT_BF16)   // TF32, and F32 as the tf32 kind over 3 rows per pair (3xTF32)
     return make_plan_impl<true>(pl, M, N, KP * rows_per_sample(dtype), G, W, ldw, max_ctas, bias,

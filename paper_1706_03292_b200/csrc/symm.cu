@@ -877,7 +877,7 @@ int symm_pack_mc(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t in_dtype, 
   PackArgs a{};
   a.u = u; a.v = v;
   a.M = M; a.N = N; a.Mp = m_pad(M); a.R = R;
-  a.K = K * rows_per_sample(dtype); a.Kp = K; a.split = dtype == POS_DT_F32;
+  a.K = K * rows_per_sample(dtype); a.Kp = K; a.split = rows_per_sample(dtype) == 3;
   a.P = P;
   const size_t mine = (size_t)c->rank * slot_bytes;
   a.mc[0] = wb->mc + off + mine;
@@ -1120,7 +1120,7 @@ int pos_loop_fc_sync(pos_loop_fc* lf, int32_t in_dtype, const void* const* u,
   // A2 + A3: every rank packs its factors into its slot of every replica's gather buffer
   PackArgs a{};
   a.M = lf->M; a.N = lf->N; a.Mp = m_pad(lf->M); a.R = row_elems(lf->M, lf->N);
-  a.K = lf->K * rows_per_sample(lf->dtype); a.Kp = lf->K; a.split = lf->dtype == POS_DT_F32;
+  a.K = lf->K * rows_per_sample(lf->dtype); a.Kp = lf->K; a.split = rows_per_sample(lf->dtype) == 3;
   a.P = P;
   const int grid = pack_grid(lf->M, lf->N, lf->K, lf->dtype);
   for (int r = 0; r < P; ++r) {

@@ -1,6 +1,7 @@
 """C-ABI library (CPU-only checks): it loads, exports every symbol include/poseidon.h declares,
 and its pure host functions agree with the oracle BIT-EXACTLY (scheme choice, Table 1 costs,
 shard table). No compute calls (no GPU here)."""
+import os
 import re
 from fractions import Fraction
 
@@ -120,7 +121,7 @@ def test_factor_row_layout():
     # 3xTF32 (reading S16): F32 packs three rows per factor pair
     assert pos.pos_factor_slot_rows(32, pos.POS_DT_BF16) == 32
     assert pos.pos_factor_slot_rows(32, pos.POS_DT_TF32) == 32
-    assert pos.pos_factor_slot_rows(32, pos.POS_DT_F32) == 96
+    assert pos.pos_factor_slot_rows(32, pos.POS_DT_F32) == (32 if os.environ.get("POS_F32_FFMA") == "1" else 96)
     assert pos.lib().pos_factor_slot_rows(1, 7) == pos.POS_EINVAL
 
 
