@@ -190,9 +190,9 @@ static int ctx_common_init(pos_ctx* c) {
   if (const char* e = getenv("POS_COMM_PRIO")) prio = std::max(hi, std::min(lo, lo - atoi(e)));
   POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio));
   c->lane_stream[0] = c->comm_stream;
-  c->ps_lanes = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxLanes, env_int("POS_PS_LANES", 1)));
-  if (c->ps_lanes > 1)
-    POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->lane_stream[1], cudaStreamNonBlocking, prio));
+  // POS_PS_LANES = 1 / 2 forces the lane count; unset (0): each scheduler decides (pos_sched_begin)
+  c->ps_lanes = (int)std::max<int64_t>(0, std::min<int64_t>(kMaxLanes, env_int("POS_PS_LANES", 0)));
+  POS_CUDA_TRY(cudaStreamCreateWithPriority(&c->lane_stream[1], cudaStreamNonBlocking, prio));
   // watchdog error word: host-mapped, so the host reads it without synchronising
   int* h = nullptr;
   POS_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h), sizeof(int), cudaHostAllocMapped));

@@ -16,7 +16,7 @@ struct pos_ctx {
   // its own cross-GPU barrier slots / epoch, so units of different lanes overlap while each lane
   // stays stream-ordered (POS_PS_LANES; the scheduler assigns lanes by unit registration order)
   cudaStream_t lane_stream[2] = {nullptr, nullptr};   // [0] = comm_stream
-  int ps_lanes = 1;
+  int ps_lanes = 0;    // 1 / 2 forced (POS_PS_LANES), 0 = the scheduler decides
   int max_ctas = 0;
   void* ws = nullptr;    // one-shot workspace (grow-only)
   size_t ws_bytes = 0;

@@ -113,6 +113,7 @@ struct pos_sched {
   // -4%, but VGG19-22K +7% and AlexNet +17% (the packs gate the reconstructions there and slow
   // down next to the PS kernels) — off by default
   int pack_stream = -1;     // flag-mode packs on pool[5]: 1 / 0 forced (POS_PACK_STREAM), -1 auto
+  int lanes = 0;           // PS lanes in use (decided at the first begin unless the context forces it)
   bool defer_exit = true;   // POS_PS_DEFER=0: the fused PS kernels wait at their exit barrier
   int n_sfb = 0;              // SFB units registered
   bool any_pair = false;      // some SFB unit reconstructs with the CTA-pair kernel
@@ -264,7 +265,7 @@ int issue_unit(pos_sched* s, int ui) {
   // with the first dense unit instead of queueing behind every factor pack of the step
   if (coll && un.scheme == POS_SCHEME_SFB && un.flag_mode && s->pack_stream == 1) cs = s->pool[5];
   // PS units alternate between the context's lanes by registration order (identical on every rank)
-  const int lane = (coll && un.scheme != POS_SCHEME_SFB && c->ps_lanes > 1) ? un.seq % c->ps_lanes : 0;
+  const int lane = (coll && un.scheme != POS_SCHEME_SFB && s->lanes > 1) ? un.seq % s->lanes : 0;
   if (lane > 0) cs = c->lane_stream[lane];
   for (int l : un.members) POS_CUDA_TRY(cudaStreamWaitEvent(cs, s->layers[l].ev_in, 0));
   // the stage that WRITES W waits for b^l to have finished reading it (WAR)
@@ -616,6 +617,19 @@ int pos_sched_begin(pos_sched* s, float alpha) {
       else t_ps += 8.0 * (P - 1.0) / P * (double)un.n / kNvlBps;
     }
     s->pack_stream = t_ps > t_sfb ? 1 : 0;
+  }
+  if (s->lanes == 0) {
+    // Two PS lanes pay off only when the PS units dominate the step: P = 4 Inception-V3 -6% (SFB
+    // parameters 0.12x the PS ones), but VGG19 +22% (6x), VGG19-22K +10% (10x) — the second lane's
+    // units then slow the reconstructions
+    int n_ps = 0;
+    double t_ps = 0.0, t_sfb = 0.0;
+    for (const auto& un : s->units) {
+      if (un.scheme == POS_SCHEME_SFB) t_sfb += 8.0 * (double)un.M * (double)un.N;
+      else { t_ps += 8.0 * (double)un.n; ++n_ps; }
+    }
+    s->lanes = s->ctx->ps_lanes > 0 ? s->ctx->ps_lanes
+                                    : ((n_ps >= 4 && t_sfb < 0.5 * t_ps) ? 2 : 1);
   }
   for (auto& ly : s->layers) ly.triggered = false;   // C := 0
   for (auto& un : s->units) un.pending = (int)un.members.size();
