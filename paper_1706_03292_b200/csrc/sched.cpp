@@ -609,8 +609,10 @@ int pos_sched_begin(pos_sched* s, float alpha) {
     // starts at once (measured, P = 2 / 4: VGG19 -9% / -5%, Inception-V3 -5% / -4%); otherwise
     // they stay ahead of the PS units so every reconstruction can start early (VGG19-22K +2% / +5%,
     // AlexNet +14% / +25% with the packs moved). Rank-invariant: registered units only.
-    constexpr double kNvlBps = 500e9, kHbmBps = 6551e9;   // per direction (measured, P = 2..4)
+    // per-direction NVLink rate of the fused PS units / NCCL (profiles/nvlink_peaks.json: 452 GB/s
+    // at P = 2, 671 at P = 4; P = 8 unmeasured, taken as P = 4's) and the measured HBM copy rate
     const double P = (double)s->ctx->world;
+    const double kNvlBps = s->ctx->world == 2 ? 452e9 : 671e9, kHbmBps = 6551e9;
     double t_ps = 0.0, t_sfb = 0.0;
     for (const auto& un : s->units) {
       if (un.scheme == POS_SCHEME_SFB) t_sfb += 8.0 * (double)un.M * (double)un.N / kHbmBps;
