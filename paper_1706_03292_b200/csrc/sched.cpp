@@ -108,10 +108,9 @@ struct pos_sched {
   int last_sfb = -1;       // most recently issued SFB unit of this iteration
   bool ps_after_sfb = false;  // P > 1: dense units wait for the SFB reconstructions (no overlap)
   int sfb_streams = 2;        // reconstruction streams (POS_SFB_STREAMS=1|2|3)
-  // flag-mode packs on their own stream (POS_PACK_STREAM=1) instead of the comm stream: the PS
-  // chain then starts with the first dense unit. Measured at P = 2 (round 2): VGG19 -7%, IncV3
-  // -4%, but VGG19-22K +7% and AlexNet +17% (the packs gate the reconstructions there and slow
-  // down next to the PS kernels) — off by default
+  // flag-mode packs on their own stream instead of the comm stream: the PS chain then starts with
+  // the first dense unit, but the packs (and so the reconstructions) wait behind PS traffic —
+  // decided per step mix at the first begin (pos_sched_begin), or forced by POS_PACK_STREAM
   int pack_stream = -1;     // flag-mode packs on pool[5]: 1 / 0 forced (POS_PACK_STREAM), -1 auto
   int lanes = 0;           // PS lanes in use (decided at the first begin unless the context forces it)
   bool defer_exit = true;   // POS_PS_DEFER=0: the fused PS kernels wait at their exit barrier
