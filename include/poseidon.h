@@ -277,6 +277,13 @@ int pos_sim_sync_layer_ps(pos_ctx* ctx, int64_t n, const float* const* grads, fl
  * PS: for r = 0..P-1, rank r reduces grads[0..P-1] on its shard in rank order, applies
  * W[r][shard] += alpha * sum, and stores the result into the shard of every W[p]. grads[p], W[p]:
  * device fp32, 16-byte aligned, >= pos_padded_size(n, P) elements. */
+/* PS over the copy engines (POS_PS_CE, the scheduler's option): the same signal / apply / wait kernels
+ * and device-to-device copies as the multi-GPU path, phase by phase over the P replicas (every
+ * rank's gradient pieces pushed into its peers' receive slots, every rank's rank-order apply, every
+ * fresh shard pushed into every replica, every completion wait). Same arguments and result as
+ * pos_loop_sync_layer_ps (bitwise: the same rank-order sum). */
+int pos_loop_sync_layer_ps_ce(pos_ctx* ctx, int64_t n, float* const* grads, float* const* W,
+                              float alpha, void* stream);
 int pos_loop_sync_layer_ps(pos_ctx* ctx, int64_t n, float* const* grads, float* const* W,
                            float alpha, void* stream);
 /* SFB: a loopback FC layer with P replicas W[p] (M x N fp32 row-major, 16-byte

@@ -284,6 +284,14 @@ class Context:
         wp = (C.c_void_p * len(Ws))(*[w.data_ptr() for w in Ws])
         _chk(lib().pos_loop_sync_layer_ps(self.h, n, gp, wp, alpha, _stream(stream)), "pos_loop_sync_layer_ps")
 
+    def loop_sync_layer_ps_ce(self, n, grads, Ws, alpha=1.0, stream=None):
+        """pos_loop_sync_layer_ps_ce: the copy-engine PS unit's kernels over P simulated replicas."""
+        assert self.local and len(grads) == len(Ws) == self.world
+        gp = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        wp = (C.c_void_p * len(Ws))(*[w.data_ptr() for w in Ws])
+        _chk(lib().pos_loop_sync_layer_ps_ce(self.h, n, gp, wp, alpha, _stream(stream)),
+             "pos_loop_sync_layer_ps_ce")
+
     def sim_sync_layer_ps(self, grads, W, alpha=1.0, n=None, stream=None):
         assert self.local and len(grads) == self.world
         n = W.numel() if n is None else n

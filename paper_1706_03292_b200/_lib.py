@@ -51,6 +51,7 @@ SIGNATURES = {
     "pos_sim_sync_layer_sfb": (C.c_int, [vp, i64, i64, i64, i32, i32, C.POINTER(vp), C.POINTER(vp),
                                          vp, vp, f32, vp]),
     "pos_sim_sync_layer_ps": (C.c_int, [vp, i64, C.POINTER(vp), vp, f32, vp]),
+    "pos_loop_sync_layer_ps_ce": (C.c_int, [vp, i64, C.POINTER(vp), C.POINTER(vp), f32, vp]),
     "pos_loop_sync_layer_ps": (C.c_int, [vp, i64, C.POINTER(vp), C.POINTER(vp), f32, vp]),
     "pos_loop_fc_create": (C.c_int, [vp, i64, i64, i64, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "pos_loop_fc_sync": (C.c_int, [vp, i32, C.POINTER(vp), C.POINTER(vp), f32, vp]),

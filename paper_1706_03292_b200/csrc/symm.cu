@@ -1041,6 +1041,84 @@ int pos_loop_sync_layer_ps(pos_ctx* c, int64_t n, float* const* grads, float* co
   return POS_OK;
 }
 
+int pos_loop_sync_layer_ps_ce(pos_ctx* c, int64_t n, float* const* grads, float* const* W,
+                              float alpha, void* stream) {
+  clear_error();
+  POS_CHECK_ARG(c && c->local, "pos_loop_* needs a context from pos_init_local");
+  POS_CHECK_ARG(n >= 1 && grads && W, "bad arguments");
+  const int P = c->world;
+  POS_CHECK_ARG(P <= kMaxPeers, "at most %d loopback ranks", kMaxPeers);
+  for (int p = 0; p < P; ++p)
+    POS_CHECK_ARG(grads[p] && W[p] && aligned16(grads[p]) && aligned16(W[p]),
+                  "rank %d: grad and W must be non-NULL and 16-byte aligned", p);
+  int rc = ctx_check(c);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t S = pos_shard_stride(n, P);
+  const size_t bytes = (size_t)symm_ce_bytes(n, P);   // one replica's receive window
+  void* ws = nullptr;
+  if ((rc = ctx_workspace(c, bytes * P, &ws))) return rc;
+  std::vector<char*> rb(P);
+  for (int p = 0; p < P; ++p) {
+    rb[p] = static_cast<char*>(ws) + bytes * p;
+    POS_CUDA_TRY(cudaMemsetAsync(rb[p], 0, kCeHdr, s));   // flags (the workspace is shared)
+  }
+  auto flag = [&](int q, int row, int r) { return reinterpret_cast<uint32_t*>(rb[q] + 128 * row) + r; };
+  clear_stale_launch_error();
+  // The copy-engine PS unit of every rank, phase by phase (a rank's apply waits for every peer's
+  // push, so the ranks cannot simply run one after the other): pushes + signals, applies, shard
+  // pushes + signals, completion waits — the kernels and copies symm_ps_ce issues per rank.
+  for (int r = 0; r < P; ++r) {
+    CeSignal sg{};
+    for (int q = 0; q < P; ++q) {
+      sg.peer[q] = flag(q, 0, r);
+      int64_t lo = 0, hi = 0;
+      pos_shard_range(n, P, q, &lo, &hi);
+      if (q != r && hi > lo)
+        POS_CUDA_TRY(cudaMemcpyAsync(rb[q] + kCeHdr + 4 * (size_t)(r * S), grads[r] + lo,
+                                     4 * (size_t)(hi - lo), cudaMemcpyDeviceToDevice, s));
+    }
+    sg.P = P;
+    sg.rank = r;
+    ce_signal_kernel<<<1, 32, 0, s>>>(sg);
+  }
+  for (int r = 0; r < P; ++r) {
+    CeApply a{};
+    a.g = grads[r];
+    a.recv = reinterpret_cast<const float*>(rb[r] + kCeHdr);
+    a.W = W[r];
+    a.flag = flag(r, 0, 0);
+    a.S = S;
+    pos_shard_range(n, P, r, &a.lo, &a.hi);
+    a.P = P;
+    a.rank = r;
+    a.alpha = alpha;
+    a.timeout_ns = c->timeout_ns;
+    a.err = c->err_dev;
+    ce_apply_kernel<<<std::max(1, ps_apply_grid(a.hi - a.lo)), 256, 0, s>>>(a);
+  }
+  for (int r = 0; r < P; ++r) {
+    int64_t lo = 0, hi = 0;
+    pos_shard_range(n, P, r, &lo, &hi);
+    CeSignal sg{};
+    for (int q = 0; q < P; ++q) {
+      sg.peer[q] = flag(q, 1, r);
+      if (q != r && hi > lo)
+        POS_CUDA_TRY(cudaMemcpyAsync(W[q] + lo, W[r] + lo, 4 * (size_t)(hi - lo),
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+    sg.reset = flag(r, 0, 0);
+    sg.P = P;
+    sg.rank = r;
+    ce_signal_kernel<<<1, 32, 0, s>>>(sg);
+  }
+  for (int r = 0; r < P; ++r)
+    ce_wait_kernel<<<1, 32, 0, s>>>(flag(r, 1, 0), P, r, c->timeout_ns, c->err_dev);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_cuda_fail(c, e, "copy-engine PS kernels (loopback)");
+  return POS_OK;
+}
+
 int pos_loop_fc_create(pos_ctx* c, int64_t M, int64_t N, int64_t K, int32_t dtype,
                        float* const* W, float* const* b, pos_loop_fc** out) {
   clear_error();

@@ -62,6 +62,44 @@ def test_loop_ps_exact_bitwise_all_replicas(P, n):
     assert len({digest(W[:n]) for W in Ws}) == 1
 
 
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [1, 4097, 16400, 590080])
+def test_loop_ps_copy_engine_exact_and_equal_to_fused(P, n):
+    """The copy-engine PS unit (POS_PS_CE: push pieces -> signal -> rank-order apply -> push shard ->
+    signal -> wait) over P replicas: bitwise equal to the oracle in the exact regime over 3
+    iterations, and to the fused kernel's rank-order result in the statistical regime."""
+    a = si.EXACT_ALPHA
+    gs = [si.exact_dense_grad(si.rng(84, n % 97, p), n) for p in range(P)]
+    w0 = si.exact_weights(si.rng(85, n % 89), n)
+    Pn = pos.pos_padded_size(n, P)
+    Ws = [torch.zeros(Pn, device="cuda") for _ in range(P)]
+    Gs = [torch.zeros(Pn, device="cuda") for _ in range(P)]
+    for p in range(P):
+        Ws[p][:n] = to_dev(w0)
+        Gs[p][:n] = to_dev(gs[p])
+    ref = w0
+    for _ in range(3):
+        ctx(P).loop_sync_layer_ps_ce(n, Gs, Ws, a)
+        ref = sync.ps_update(ref, gs, a)
+    torch.cuda.synchronize()
+    assert ctx(P).async_error() == 0
+    for p in range(P):
+        assert np.array_equal(to_host(Ws[p][:n]), ref), (P, n, p)
+    gs = [si.stat_dense_grad(si.rng(86, 0, p), n) for p in range(P)]
+    w0 = si.stat_weights(si.rng(87), 1, n)[0]
+    outs = []
+    for fn in (ctx(P).loop_sync_layer_ps_ce, ctx(P).loop_sync_layer_ps):
+        Ws = [torch.zeros(Pn, device="cuda") for _ in range(P)]
+        Gs = [torch.zeros(Pn, device="cuda") for _ in range(P)]
+        for p in range(P):
+            Ws[p][:n] = to_dev(w0)
+            Gs[p][:n] = to_dev(gs[p])
+        fn(n, Gs, Ws, -0.01 / P)
+        torch.cuda.synchronize()
+        outs.append([digest(W[:n]) for W in Ws])
+    assert len(set(outs[0])) == 1 and outs[0] == outs[1]
+
+
 @pytest.mark.parametrize("P", [2, 8])
 def test_loop_ps_statistical_and_repeatable(P):
     n = 2359808 + 64 * 3 + 5
