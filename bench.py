@@ -56,15 +56,15 @@ NVLINK_GBS_PER_DIR = 770.0   # measured peer copy per direction (B200_PROFILING.
 
 def load_nvlink(P):
     """Achievable per-direction NVLink bandwidth for P GPUs, measured by scripts/nvlink_peaks.py
-    (nccl-tests style AG / RS busbw, profiles/nvlink_peaks.json); else the guide's peer-copy
-    figure."""
+    (nccl-tests style AG / RS busbw and the fused PS unit, plus — at P = 2 — copy-engine peer copies;
+    profiles/nvlink_peaks.json); else the guide's peer-copy figure."""
     p = os.path.join(ROOT, "profiles", "nvlink_peaks.json")
     if P > 1 and os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
         key = f"P{P}"
         if key in d:
-            return float(d[key]["per_dir_gbs"]), f"measured (profiles/nvlink_peaks.json {key}: max NCCL AG/RS busbw)"
+            return float(d[key]["per_dir_gbs"]), f"measured (profiles/nvlink_peaks.json {key}: max of NCCL AG/RS busbw, the fused PS unit and copy-engine copies)"
         near = sorted(d, key=lambda k: abs(int(k[1:]) - P))
         if near:
             return float(d[near[0]]["per_dir_gbs"]), f"measured at {near[0]} (profiles/nvlink_peaks.json; no {key} entry)"

@@ -512,9 +512,11 @@ int ps_grid(pos_ctx* c, int64_t n, int P) {
   // reconstructions): P = 2 wants 64 CTAs (round 1: 0.45 -> 0.41 ms; 16: 0.52, 128: 0.47); P = 4
   // is best at 24-48 and 16 CTAs cost +17% (round 2: 0.363 vs 0.426 ms). Rule: 128 / P CTAs (the
   // same shard bytes per CTA), but >= 32 so a rank keeps enough NVLS loads in flight (P = 8: 32;
-  // untested at P = 8 — the builder's boxes have at most 4 GPUs).
+  // untested at P = 8 — the builder's boxes have at most 4 GPUs). P = 2 on the round-2 close
+  // defaults (peer-load kernel, epoch barriers, pack placement): 96 CTAs beat 64 (VGG19 0.256 vs
+  // 0.268 ms, VGG19-22K 0.337 vs 0.342; 128: VGG19 bimodal, 0.33 median).
   (void)c;
-  int cap = ps_ctas_env > 0 ? ps_ctas_env : std::max(32, 128 / P);
+  int cap = ps_ctas_env > 0 ? ps_ctas_env : (P == 2 ? 96 : std::max(32, 128 / P));
   const int64_t S = pos_shard_stride(n, P);
   return grid_for(std::max<int64_t>(1, S / 4 / kPsUnroll), kPsThreads, cap);
 }
