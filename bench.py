@@ -792,7 +792,10 @@ def run_ours(a):
                       + ", all SFB layers of one step)",
             "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"] if achieved else None,
-            "traffic": traffic,
+            # per launch like `achieved` (the step's launches averaged); the step total beside it
+            "traffic": traffic / n_a4 if (traffic and n_a4) else None,
+            "traffic_per_step": traffic,
+            "algorithmic_bytes_per_launch": a4_bytes / n_a4 if n_a4 else None,
             "algorithmic_bytes_per_step": a4_bytes, "kernel_ms_per_step": a4_ms,
             "launches_per_step": n_a4, "avg_launch_ms": a4_ms / n_a4 if n_a4 else None,
             "kernel_ms_note": ("per-launch durations from CUDA events around each apply stage inside the "
