@@ -49,7 +49,8 @@ enum { POS_ROLE_SERVER = 0, POS_ROLE_WORKER = 1, POS_ROLE_BOTH = 2 };
 /* Factor COMPUTE dtype of the SFB reconstruction (what is gathered and fed to the contraction):
  *   BF16: factors rounded to bf16 (RNE), tcgen05 kind::f16, fp32 accumulate in TMEM.
  *   TF32: factors kept fp32, tcgen05 kind::tf32 (tensor core rounds to tf32), fp32 accumulate.
- *   F32 : factors kept fp32, exact fp32 FFMA contraction (SIMT), fp32 accumulate. */
+ *   F32 : factors kept fp32, fp32-accurate: 3xTF32 on tcgen05 kind::tf32 (each pair split into three
+ *         tf32 rows, pos_factor_slot_rows), fp32 accumulate; POS_F32_FFMA=1: SIMT FFMA instead. */
 enum { POS_DT_BF16 = 0, POS_DT_TF32 = 1, POS_DT_F32 = 2 };
 /* Storage dtype of the caller's u / v buffers. */
 enum { POS_IN_BF16 = 0, POS_IN_F32 = 1 };
