@@ -41,11 +41,19 @@ METRIC = "grad_sync_params_per_s"
 UNIT = "params/s"
 
 
-def default_bucket_mb(P):
+def default_bucket_mb(P, model=None):
     """PS unit size of the timed plan (--bucket-mb default), as measured on VGG19-22K (round 2):
     P = 1: 16 MiB (local applies; 64 MiB +0.8%); P = 2: 64 MiB (each fused cross-GPU unit costs
     ~17 us of fixed latency and the PS chain is exposed: 0.338 vs 0.375 ms with 16 MiB); P >= 4:
-    16 MiB (0.366 vs 0.412 ms with 64 MiB — the big unit, issued last, ends the step)."""
+    16 MiB (0.366 vs 0.412 ms with 64 MiB — the big unit, issued last, ends the step).
+    A model whose PS (dense) parameters dominate — FC parameters under half the dense ones, the
+    scheduler's two-lane rule — takes 32 MiB at P = 2: four units, so two PS lanes (Inception-V3
+    0.208 -> 0.189 ms; VGG19 / VGG19-22K are slower with 32 MiB: 0.264 / 0.338 ms)."""
+    if P == 2 and model is not None:
+        fc = sum(l.M * l.N for l in model.layers if l.kind == "fc")
+        dense = sum(l.params for l in model.layers if l.kind != "fc")
+        if fc < 0.5 * dense:
+            return 32.0
     return 64.0 if P == 2 else 16.0
 
 
@@ -479,7 +487,7 @@ def run_ours(a):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * 1 + rank)
     if a.bucket_mb is None:
-        a.bucket_mb = default_bucket_mb(P)
+        a.bucket_mb = default_bucket_mb(P, model)
     units = plan_units(model, int(a.bucket_mb * 2 ** 20 / 4))
     # The timed region replays UNTRACED step graphs. In-step kernel times come from a second ring
     # of the same step captured with device-side tracing (the kernels stamp %globaltimer; no timing
