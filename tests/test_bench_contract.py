@@ -30,3 +30,15 @@ def test_bench_rejects_too_few_warmup_steps():
                         "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300,
                        cwd=ROOT)
     assert p.returncode != 0 and "--warmup must be >= 3" in p.stderr
+
+
+def test_default_bucket_plan():
+    """bench.py's PS unit size: 16 MiB at P = 1 and P >= 4; at P = 2 64 MiB, or 32 MiB when the
+    dense parameters dominate (FC < half of dense: Inception-V3)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth_inputs as si
+    for cfg, p2 in (("c1", 64.0), ("c2", 64.0), ("c3", 64.0), ("c4", 32.0)):
+        model = si.load_model(si.CONFIGS[cfg][0])
+        assert [bench.default_bucket_mb(P, model) for P in (1, 2, 4, 8)] == [16.0, p2, 16.0, 16.0], cfg
+    assert bench.default_bucket_mb(2) == 64.0 and bench.DEFAULT_BUCKET_MB == 16.0
